@@ -1,0 +1,211 @@
+/* psm.h — C-ABI of the B200 surfel rasterizer (Ψ-Map render hot path).
+ *
+ * This is the drop-in boundary for `psimap::render` / `render_into` /
+ * `bench_render` (reference: proj/include/psimap/raster.hpp:142-172,
+ * proj/src/raster.cpp:266-573). No torch, no C++ types, no exceptions cross
+ * it: plain pointers and sizes, int status codes. The C++ drop-in shim with the
+ * reference's own names and types sits on top of it (include/psimap_b200.hpp).
+ *
+ * Buffer layouts are the reference's (proj/include/psimap/core_types.hpp:17-53,
+ * proj/include/psimap/image.hpp:11-43):
+ *   surfels13  N x 13 doubles, AoS, per surfel: center[3], rotation (w,x,y,z)[4],
+ *              scales[2], opacity, color[3]   (Surfel, core_types.hpp:17-25)
+ *   f_sem      N x C_sem doubles, row-major (Surfel::f_sem of every surfel;
+ *              C_sem taken from surfel 0 like SceneMap::c_sem, core_types.hpp:108)
+ *   labels     N x N_q doubles, surfel-major: the column-major Eigen MatX
+ *              N_q x N passed as `const MatX* labels` (raster.hpp:142), so each
+ *              surfel's distribution is contiguous (raster.cpp:337,352). May be NULL.
+ *   planes     W x H x C, row-major, channel fastest: data[(y*W + x)*C + c]
+ *              (Plane<T>, image.hpp:11-43). Written as fp32 / int32.
+ *
+ * Thread-safety: a context is used by one host thread at a time; distinct
+ * contexts (one per device) are independent (reference render is reentrant,
+ * raster.hpp:147).
+ */
+#ifndef PSM_H
+#define PSM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define PSM_OK 0
+#define PSM_EINVAL 1       /* bad argument, or a degenerate quaternion on a surfel that passed
+                              the depth cull: mirrors std::invalid_argument thrown by
+                              rotation_from_quat (proj/src/math_util.cpp:46-50) inside
+                              project_surfel (proj/src/raster.cpp:99) */
+#define PSM_ENOMEM 2
+#define PSM_ECUDA 3
+#define PSM_EUNSUPPORTED 4 /* valid for the reference, not implemented on the GPU path */
+
+typedef struct psm_ctx psm_ctx;
+typedef struct psm_scene psm_scene;
+
+/* Camera (proj/include/psimap/core_types.hpp:36-53). r_cw is column-major like
+ * Eigen::Matrix3d: r_cw[col*3 + row]. */
+typedef struct psm_camera {
+  double r_cw[9];
+  double t_cw[3];
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double near_clip, far_clip;
+} psm_camera;
+
+/* Binning (raster.hpp:17 adds Ellipse): CIRCLE = bin_circle (raster.cpp:144-147),
+ * AABB = bin_aabb (raster.cpp:149-152), ELLIPSE = the exact support-ellipse vs
+ * tile test (north-star "Precise Tile Intersection"; a subset of AABB's lists
+ * that leaves every output plane unchanged; falls back to AABB when
+ * support_cutoff == 0). */
+enum { PSM_BIN_CIRCLE = 0, PSM_BIN_AABB = 1, PSM_BIN_ELLIPSE = 2 };
+/* Blending (raster.hpp:18) */
+enum { PSM_BLEND_FULL = 0, PSM_BLEND_TOPK = 1 };
+
+/* RasterConfig (proj/include/psimap/raster.hpp:42-54). Defaults via
+ * psm_default_config(). The GPU path requires tile_size == 16. */
+typedef struct psm_raster_config {
+  int32_t tile_size;
+  double chi2;
+  double alpha_min;
+  double t_min;
+  int32_t support_cutoff;
+  int32_t binning;
+  int32_t blending;
+  int32_t top_k;            /* effective K = max(top_k, 1) (raster.cpp:318); GPU K <= 32 */
+  double background[3];
+  int32_t render_depth_normal;
+  int32_t threads;          /* host worker count in the reference; ignored on the GPU */
+} psm_raster_config;
+
+/* RenderTargets (raster.hpp:56-66) as fp32/int32 planes. Any pointer may be
+ * NULL to skip that plane's write-back (the plane is still computed on the
+ * device). on_device = 1: pointers are device memory of the context's device
+ * and the render is asynchronous on the context stream; 0: host memory, the
+ * call copies back and synchronises. */
+typedef struct psm_targets {
+  float* color;        /* W*H*3 */
+  float* depth;        /* W*H*2: expected depth, dominant-surfel depth */
+  float* normal;       /* W*H*3 */
+  float* sem_feat;     /* W*H*C_sem */
+  float* ins_dist;     /* W*H*N_q */
+  int32_t* ins_argmax; /* W*H, -1 where nothing accumulated */
+  float* alpha_acc;    /* W*H */
+  int32_t* blend_count;/* W*H */
+  int32_t on_device;
+} psm_targets;
+
+/* Counters: TileGrid::rn_total / rn_per_tile (raster.hpp:36-37),
+ * RenderTargets::blended_total (raster.hpp:65), plus the projected count. */
+typedef struct psm_counters {
+  uint64_t rn_total;
+  double rn_per_tile;
+  uint64_t blended_total;
+  int64_t n_proj;
+  int32_t tiles_x, tiles_y;
+  int64_t nonempty_tiles;
+} psm_counters;
+
+/* Debug export for the parity suite (host pointers, caller-owned; any may be NULL).
+ *   tile_keys   [cap_keys] sorted (tile << 32 | depth rank) keys
+ *   tile_vals   [cap_keys] source surfel index of each key (the tile lists of
+ *               TileGrid::tiles, raster.hpp:35, as scene indices)
+ *   tile_ranges [2 * tiles] [start, end) of each tile in tile_keys
+ *   depth_order [cap_proj]  source index at each depth rank ((sort_depth, source)
+ *               order of raster.cpp:78-83)
+ *   topk_src    [W*H*K] selected source indices per pixel in blend order, -1 padded
+ *               (topk_select, raster.cpp:225-251 + compaction 438-454); written
+ *               when blending == TOPK. */
+typedef struct psm_debug {
+  uint64_t* tile_keys;
+  int32_t* tile_vals;
+  int64_t cap_keys;
+  int32_t* tile_ranges;
+  int32_t* depth_order;
+  int64_t cap_proj;
+  int32_t* topk_src;
+} psm_debug;
+
+/* Stage timings of the last render when profiling is on (CUDA events on the
+ * context stream), milliseconds. */
+typedef struct psm_stage_times {
+  float preprocess;   /* K1: project_surfel + hot-record build (raster.cpp:94-142,321-353) */
+  float depth_sort;   /* K2: (sort_depth, source) order (raster.cpp:78-83) */
+  float emit;         /* K3/K4: per-surfel tile counts, scan, key emission (raster.cpp:59-74) */
+  float tile_sort;    /* K5: stable sort by tile */
+  float ranges;       /* K6: per-tile [start,end) + counters (raster.cpp:84-88) */
+  float blend;        /* K7: per-pixel compositing + Top-K + features (raster.cpp:355-506) */
+  float total;
+} psm_stage_times;
+
+void psm_default_config(psm_raster_config* cfg);
+
+/* Context: one per device; owns a stream (or borrows `stream` if non-NULL, a
+ * cudaStream_t) and grow-only scratch arenas reused across frames (the
+ * render_into buffer-reuse contract, raster.cpp:255-262). */
+int psm_create(int device, void* stream, psm_ctx** out);
+int psm_destroy(psm_ctx* ctx);
+const char* psm_last_error(const psm_ctx* ctx);
+int psm_set_profiling(psm_ctx* ctx, int enabled);
+int psm_get_stage_times(const psm_ctx* ctx, psm_stage_times* out);
+int psm_sync(psm_ctx* ctx);
+
+/* Upload a scene once (the SceneMap + labels the reference borrows by const&
+ * per call, raster.hpp:142-148). Geometry stays fp64 on the device for
+ * bit-exact decisions; features and labels are stored fp32. */
+int psm_scene_upload(psm_ctx* ctx, const double* surfels13, int64_t n, const double* f_sem,
+                     int32_t c_sem, const double* labels, int32_t n_q, psm_scene** out);
+int psm_scene_free(psm_ctx* ctx, psm_scene* scene);
+int psm_scene_info(const psm_scene* scene, int64_t* n, int32_t* c_sem, int32_t* n_q);
+
+/* render_into (raster.cpp:273-511). counters may be NULL. With on_device
+ * targets and counters == NULL the call is asynchronous. */
+int psm_render(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam,
+               const psm_raster_config* cfg, const psm_targets* targets, psm_counters* counters);
+
+/* Same render plus the debug export of sorted keys, tile ranges, depth order and Top-K ids. */
+int psm_render_debug(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam,
+                     const psm_raster_config* cfg, const psm_targets* targets,
+                     psm_counters* counters, psm_debug* debug);
+
+/* n_views independent renders (one per camera) into n_views target sets;
+ * views share the scene upload. counters may be NULL or an array of n_views. */
+int psm_render_batch(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cams, int32_t n_views,
+                     const psm_raster_config* cfg, const psm_targets* targets,
+                     psm_counters* counters);
+
+/* Counters of the most recent render, valid after psm_sync. */
+int psm_last_counters(const psm_ctx* ctx, psm_counters* out);
+
+/* Workload: make_street_scene (proj/src/synthetic.cpp:236-312) with the same
+ * RNG draw order, plus `scale_mult` applied to s1 after it is drawn
+ * (density-normalised variants; 1.0 = verbatim). Two-phase:
+ * call with NULL outputs to get n; then with buffers of n*13, n*c_sem and (if
+ * labels != NULL) n*n_instances doubles. The camera is the reference's
+ * look_at((0,0,0) -> (0,0,20), up (0,-1,0), f = 0.8 W, near 0.1, far 200). */
+typedef struct psm_street_spec {
+  int32_t n_surfels;
+  uint64_t seed;
+  double min_aspect;
+  int32_t image_w, image_h;
+  int32_t c_sem;
+  int32_t n_instances;
+  double scale_mult;
+} psm_street_spec;
+int psm_make_street_scene(const psm_street_spec* spec, int64_t* n_out, double* surfels13,
+                          double* f_sem, double* labels, psm_camera* cam);
+
+/* Camera::look_at / Camera::make (proj/src/core_types.cpp:18-60). */
+int psm_camera_look_at(const double eye[3], const double target[3], const double up[3], double fx,
+                       double fy, int32_t width, int32_t height, double near_clip,
+                       double far_clip, psm_camera* out);
+int psm_camera_make(const double r_cw[9], const double t_cw[3], double fx, double fy, double cx,
+                    double cy, int32_t width, int32_t height, double near_clip, double far_clip,
+                    psm_camera* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSM_H */

@@ -1,0 +1,68 @@
+"""ctypes mirrors of the structs in include/psm.h (no library is loaded here).
+
+Kept separate from `_lib` so the test-side oracle wrapper can share the exact
+struct layouts without loading the CUDA library.
+"""
+import ctypes as C
+
+PSM_OK = 0
+PSM_EINVAL = 1
+PSM_ENOMEM = 2
+PSM_ECUDA = 3
+PSM_EUNSUPPORTED = 4
+
+BIN_CIRCLE, BIN_AABB, BIN_ELLIPSE = 0, 1, 2
+BLEND_FULL, BLEND_TOPK = 0, 1
+
+
+class psm_camera(C.Structure):
+    _fields_ = [("r_cw", C.c_double * 9), ("t_cw", C.c_double * 3), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("width", C.c_int32), ("height", C.c_int32),
+                ("near_clip", C.c_double), ("far_clip", C.c_double)]
+
+
+class psm_raster_config(C.Structure):
+    _fields_ = [("tile_size", C.c_int32), ("chi2", C.c_double), ("alpha_min", C.c_double), ("t_min", C.c_double),
+                ("support_cutoff", C.c_int32), ("binning", C.c_int32), ("blending", C.c_int32), ("top_k", C.c_int32),
+                ("background", C.c_double * 3), ("render_depth_normal", C.c_int32), ("threads", C.c_int32)]
+
+
+class psm_targets(C.Structure):
+    _fields_ = [("color", C.c_void_p), ("depth", C.c_void_p), ("normal", C.c_void_p), ("sem_feat", C.c_void_p),
+                ("ins_dist", C.c_void_p), ("ins_argmax", C.c_void_p), ("alpha_acc", C.c_void_p),
+                ("blend_count", C.c_void_p), ("on_device", C.c_int32)]
+
+
+class psm_counters(C.Structure):
+    _fields_ = [("rn_total", C.c_uint64), ("rn_per_tile", C.c_double), ("blended_total", C.c_uint64),
+                ("n_proj", C.c_int64), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("nonempty_tiles", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class psm_debug(C.Structure):
+    _fields_ = [("tile_keys", C.c_void_p), ("tile_vals", C.c_void_p), ("cap_keys", C.c_int64),
+                ("tile_ranges", C.c_void_p), ("depth_order", C.c_void_p), ("cap_proj", C.c_int64),
+                ("topk_src", C.c_void_p)]
+
+
+class psm_stage_times(C.Structure):
+    _fields_ = [("preprocess", C.c_float), ("depth_sort", C.c_float), ("emit", C.c_float), ("tile_sort", C.c_float),
+                ("ranges", C.c_float), ("blend", C.c_float), ("total", C.c_float)]
+
+    def as_dict(self):
+        return {k: float(getattr(self, k)) for k, _ in self._fields_}
+
+
+class psm_street_spec(C.Structure):
+    _fields_ = [("n_surfels", C.c_int32), ("seed", C.c_uint64), ("min_aspect", C.c_double), ("image_w", C.c_int32),
+                ("image_h", C.c_int32), ("c_sem", C.c_int32), ("n_instances", C.c_int32), ("scale_mult", C.c_double)]
+
+
+# Every symbol include/psm.h declares (checked by tests/test_capi_symbols.py).
+EXPORTED_SYMBOLS = (
+    "psm_default_config", "psm_create", "psm_destroy", "psm_last_error", "psm_set_profiling", "psm_get_stage_times",
+    "psm_sync", "psm_scene_upload", "psm_scene_free", "psm_scene_info", "psm_render", "psm_render_debug",
+    "psm_render_batch", "psm_last_counters", "psm_make_street_scene", "psm_camera_look_at", "psm_camera_make",
+)

@@ -1,0 +1,585 @@
+// capi.cu — the C-ABI (include/psm.h): contexts, scene upload and the
+// per-frame render pipeline K1..K7 on one CUDA stream.
+//
+// Reference entry points replaced: psimap::render / render_into
+// (proj/src/raster.cpp:266-511, raster.hpp:142-148). Per frame:
+//   K1 preprocess       project_surfel + hot records + box + tile count  (raster.cpp:94-142,321-353)
+//   K2 compact + sort   stable radix sort of (depth bits, source)        (raster.cpp:78-83)
+//   K3 scan             tile counts in rank order -> key offsets, RN-Total
+//   K4 emit             (tile, source) in rank order                       (raster.cpp:59-74)
+//   K5 tile sort        stable radix sort on the tile bits
+//   K6 ranges           per-tile [start, end), non-empty count             (raster.cpp:84-88)
+//   K7 blend            compositing + Top-K + features                     (raster.cpp:355-506)
+// Scratch is grow-only and owned by the context (render_into's buffer reuse,
+// raster.cpp:255-262). No CPU fallback: without a CUDA device every entry
+// point returns PSM_ECUDA.
+#include <cub/cub.cuh>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "psm_device.cuh"
+#include "psm_kernels.h"
+
+struct psm_scene {
+  int device = 0;
+  int64_t n = 0;
+  int32_t c_sem = 0, n_q = 0;
+  double* surfels = nullptr;  // N x 13 fp64
+  float* feat = nullptr;      // N x (c_sem + n_q) fp32
+};
+
+namespace psm {
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace psm
+
+struct psm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  bool profiling = false;
+  cudaEvent_t ev[8] = {};
+  int ev_next = 0;
+  psm_stage_times times{};
+  psm_counters last{};
+  // scratch
+  psm::Buf recs, bins, depth_bits, tile_cnt, valid, pos, keys_c, src_c, keys_s, src_s, cnt_rank, off_rank;
+  psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, cub_tmp, dev_small, lists, rank_of, dbg_keys, topk_dbg;
+  psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
+  int64_t* h_small = nullptr;  // pinned: counters read-back
+};
+
+namespace psm {
+namespace {
+
+int fail(psm_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+}  // namespace
+
+int fail_cuda(psm_ctx* ctx, cudaError_t e, const char* expr, const char* file, int line) {
+  char buf[512];
+  std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e), file,
+                line, expr);
+  return fail(ctx, PSM_ECUDA, buf);
+}
+
+namespace {
+
+template <class T>
+int ensure(psm_ctx* ctx, Buf& b, size_t count, T** out) {
+  const size_t bytes = count * sizeof(T) + 16;
+  if (b.bytes < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    const size_t want = bytes + bytes / 4;  // grow-only with headroom
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, PSM_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    }
+    b.bytes = want;
+  }
+  *out = static_cast<T*>(b.p);
+  return PSM_OK;
+}
+
+#define PSM_TRY(expr)            \
+  do {                           \
+    int _st = (expr);            \
+    if (_st != PSM_OK) return _st; \
+  } while (0)
+
+void free_buf(Buf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+int tile_bits(int tiles) {
+  int b = 1;
+  while ((1 << b) < tiles) ++b;
+  return b;
+}
+
+// Stage boundary i (0..6); boundaries of skipped stages are recorded at the
+// same point so they time as zero.
+void record(psm_ctx* ctx, int i) {
+  if (!ctx->profiling) return;
+  while (ctx->ev_next <= i) cudaEventRecord(ctx->ev[ctx->ev_next++], ctx->stream);
+}
+
+// Validates the subset of RasterConfig the GPU path supports.
+int check_config(psm_ctx* ctx, const psm_raster_config* cfg, int feat_dims) {
+  if (cfg->tile_size != 16) return fail(ctx, PSM_EUNSUPPORTED, "GPU path requires tile_size == 16");
+  if (cfg->binning < 0 || cfg->binning > 2) return fail(ctx, PSM_EINVAL, "binning must be 0 (circle), 1 (aabb), 2 (ellipse)");
+  if (cfg->blending < 0 || cfg->blending > 1) return fail(ctx, PSM_EINVAL, "blending must be 0 (full) or 1 (topk)");
+  const int k_sel = cfg->top_k > 1 ? cfg->top_k : 1;
+  if (cfg->blending == PSM_BLEND_TOPK && blend_kmax_for(k_sel) < 0)
+    return fail(ctx, PSM_EUNSUPPORTED, "GPU path supports top_k <= 32");
+  if (blend_nch_for(feat_dims) < 0) return fail(ctx, PSM_EUNSUPPORTED, "GPU path supports C_sem + N_q <= 512");
+  return PSM_OK;
+}
+
+struct Planes {
+  float *color, *depth, *normal, *sem, *ins, *alpha;
+  int32_t *arg, *cnt;
+};
+
+// The render proper. Leaves results in `pl` (device) and counters in ctx->last.
+int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
+                const Planes& pl, psm_debug* dbg) {
+  cudaStream_t st = ctx->stream;
+  const int64_t n = sc->n;
+  const int W = cam->width, H = cam->height;
+  const int ts = cfg->tile_size;
+  const int tiles_x = (W + ts - 1) / ts, tiles_y = (H + ts - 1) / ts;
+  const int tiles = tiles_x * tiles_y;
+  const int feat_dims = sc->c_sem + sc->n_q;
+  const bool topk = cfg->blending == PSM_BLEND_TOPK;
+  const int k_sel = cfg->top_k > 1 ? cfg->top_k : 1;
+
+  DevCamera dc;
+  std::memcpy(dc.r, cam->r_cw, sizeof dc.r);
+  std::memcpy(dc.t, cam->t_cw, sizeof dc.t);
+  dc.fx = cam->fx; dc.fy = cam->fy; dc.cx = cam->cx; dc.cy = cam->cy;
+  dc.w = W; dc.h = H; dc.near_clip = cam->near_clip; dc.far_clip = cam->far_clip;
+  DevRaster rs;
+  rs.chi2 = cfg->chi2; rs.alpha_min = cfg->alpha_min; rs.t_min = cfg->t_min;
+  rs.bg[0] = cfg->background[0]; rs.bg[1] = cfg->background[1]; rs.bg[2] = cfg->background[2];
+  rs.support_cutoff = cfg->support_cutoff != 0;
+  rs.binning = cfg->binning;
+  if (rs.binning == PSM_BIN_ELLIPSE && !rs.support_cutoff) rs.binning = PSM_BIN_AABB;  // exactness needs the cutoff
+  rs.render_depth_normal = cfg->render_depth_normal != 0;
+  rs.tile_size = ts;
+  rs.tiles_x = tiles_x; rs.tiles_y = tiles_y;
+
+  // small device counters: [0] err, [1] nonempty, [2] blended_total, [3] list overflow
+  unsigned long long* small = nullptr;
+  PSM_TRY(ensure(ctx, ctx->dev_small, 8, &small));
+  PSM_CUDA_TRY(cudaMemsetAsync(small, 0, 8 * sizeof(unsigned long long), st));
+  int32_t* ranges = nullptr;
+  PSM_TRY(ensure(ctx, ctx->ranges, static_cast<size_t>(tiles) * 2, &ranges));
+  PSM_CUDA_TRY(cudaMemsetAsync(ranges, 0, sizeof(int32_t) * 2 * tiles, st));
+
+  ctx->ev_next = 0;
+  record(ctx, 0);
+  int64_t n_proj = 0, rn = 0;
+  uint32_t* src_s = nullptr;
+  uint32_t* tvals_s = nullptr;
+  uint32_t* tkeys_s = nullptr;
+  if (n > 0) {
+    SurfRec* recs; BinRec* bins; uint64_t* dbits; int32_t *tcnt, *valid, *pos;
+    PSM_TRY(ensure(ctx, ctx->recs, n, &recs));
+    PSM_TRY(ensure(ctx, ctx->bins, n, &bins));
+    PSM_TRY(ensure(ctx, ctx->depth_bits, n, &dbits));
+    PSM_TRY(ensure(ctx, ctx->tile_cnt, n, &tcnt));
+    PSM_TRY(ensure(ctx, ctx->valid, n, &valid));
+    PSM_TRY(ensure(ctx, ctx->pos, n, &pos));
+    launch_preprocess(sc->surfels, n, dc, rs, recs, bins, dbits, tcnt, valid, reinterpret_cast<int32_t*>(small), st);
+    PSM_CUDA_TRY(cudaGetLastError());
+    record(ctx, 1);
+
+    // K2: compaction + depth sort
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, valid, pos, static_cast<int>(n), st);
+    void* tmp;
+    PSM_TRY(ensure(ctx, ctx->cub_tmp, tmp_bytes, reinterpret_cast<char**>(&tmp)));
+    PSM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, valid, pos, static_cast<int>(n), st));
+    int32_t tail[2];
+    PSM_CUDA_TRY(cudaMemcpyAsync(&tail[0], pos + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PSM_CUDA_TRY(cudaMemcpyAsync(&tail[1], valid + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    int32_t err_flag = 0;
+    PSM_CUDA_TRY(cudaMemcpyAsync(&err_flag, small, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+    if (err_flag) return fail(ctx, PSM_EINVAL, "degenerate quaternion");
+    n_proj = static_cast<int64_t>(tail[0]) + tail[1];
+    if (n_proj > 0) {
+      uint64_t *keys_c, *keys_s; uint32_t *src_c;
+      PSM_TRY(ensure(ctx, ctx->keys_c, n_proj, &keys_c));
+      PSM_TRY(ensure(ctx, ctx->src_c, n_proj, &src_c));
+      PSM_TRY(ensure(ctx, ctx->keys_s, n_proj, &keys_s));
+      PSM_TRY(ensure(ctx, ctx->src_s, n_proj, &src_s));
+      launch_compact(valid, pos, dbits, n, keys_c, src_c, st);
+      PSM_CUDA_TRY(cudaGetLastError());
+      tmp_bytes = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_c, keys_s, src_c, src_s, static_cast<int>(n_proj), 0, 63, st);
+      PSM_TRY(ensure(ctx, ctx->cub_tmp, tmp_bytes, reinterpret_cast<char**>(&tmp)));
+      PSM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_c, keys_s, src_c, src_s,
+                                                   static_cast<int>(n_proj), 0, 63, st));
+      record(ctx, 2);
+
+      // K3: tile counts in rank order, exclusive scan -> offsets, RN-Total
+      uint32_t *cnt_rank, *off_rank;
+      PSM_TRY(ensure(ctx, ctx->cnt_rank, n_proj, &cnt_rank));
+      PSM_TRY(ensure(ctx, ctx->off_rank, n_proj, &off_rank));
+      launch_gather_counts(src_s, tcnt, n_proj, cnt_rank, st);
+      tmp_bytes = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt_rank, off_rank, static_cast<int>(n_proj), st);
+      PSM_TRY(ensure(ctx, ctx->cub_tmp, tmp_bytes, reinterpret_cast<char**>(&tmp)));
+      PSM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt_rank, off_rank, static_cast<int>(n_proj), st));
+      uint32_t rtail[2];
+      PSM_CUDA_TRY(cudaMemcpyAsync(&rtail[0], off_rank + (n_proj - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      PSM_CUDA_TRY(cudaMemcpyAsync(&rtail[1], cnt_rank + (n_proj - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      PSM_CUDA_TRY(cudaStreamSynchronize(st));
+      rn = static_cast<int64_t>(rtail[0]) + rtail[1];
+      if (rn > 0x7fffffffLL) return fail(ctx, PSM_EUNSUPPORTED, "RN-Total exceeds 2^31 tile assignments");
+
+      if (rn > 0) {
+        // K4: emit (tile, source) in rank order
+        uint32_t *tkeys, *tvals, *tkeys2, *tvals2;
+        PSM_TRY(ensure(ctx, ctx->tkeys, rn, &tkeys));
+        PSM_TRY(ensure(ctx, ctx->tvals, rn, &tvals));
+        PSM_TRY(ensure(ctx, ctx->tkeys2, rn, &tkeys2));
+        PSM_TRY(ensure(ctx, ctx->tvals2, rn, &tvals2));
+        launch_emit(src_s, off_rank, n_proj, recs, bins, rs, H, tkeys, tvals, st);
+        PSM_CUDA_TRY(cudaGetLastError());
+        record(ctx, 3);
+        // K5: stable sort on the tile bits
+        tmp_bytes = 0;
+        const int tb = tile_bits(tiles);
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, tkeys, tkeys2, tvals, tvals2, static_cast<int>(rn), 0, tb, st);
+        PSM_TRY(ensure(ctx, ctx->cub_tmp, tmp_bytes, reinterpret_cast<char**>(&tmp)));
+        PSM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, tkeys, tkeys2, tvals, tvals2, static_cast<int>(rn),
+                                                     0, tb, st));
+        tkeys_s = tkeys2;
+        tvals_s = tvals2;
+        record(ctx, 4);
+        // K6: ranges
+        launch_ranges(tkeys_s, rn, ranges, small + 1, st);
+        PSM_CUDA_TRY(cudaGetLastError());
+      }
+    }
+  }
+  record(ctx, 5);
+
+  // K7: blend
+  BlendParams bp;
+  std::memset(&bp, 0, sizeof bp);
+  bp.ranges = ranges;
+  bp.vals = tvals_s;
+  bp.recs = static_cast<const SurfRec*>(ctx->recs.p);
+  bp.feat = sc->feat;
+  bp.feat_dims = feat_dims; bp.c_sem = sc->c_sem; bp.n_q = sc->n_q;
+  bp.width = W; bp.height = H; bp.tiles_x = tiles_x;
+  bp.cam_cx = cam->cx; bp.cam_cy = cam->cy; bp.cam_fx = cam->fx; bp.cam_fy = cam->fy;
+  bp.chi2 = cfg->chi2; bp.alpha_min = cfg->alpha_min; bp.t_min = cfg->t_min;
+  bp.bg0 = cfg->background[0]; bp.bg1 = cfg->background[1]; bp.bg2 = cfg->background[2];
+  bp.support_cutoff = cfg->support_cutoff != 0;
+  bp.render_depth_normal = cfg->render_depth_normal != 0;
+  bp.k_sel = k_sel;
+  bp.color = pl.color; bp.depth = pl.depth; bp.normal = pl.normal; bp.sem_feat = pl.sem; bp.ins_dist = pl.ins;
+  bp.alpha_acc = pl.alpha; bp.ins_argmax = pl.arg; bp.blend_count = pl.cnt;
+  bp.blended_total = small + 2;
+  bp.list_overflow = reinterpret_cast<int32_t*>(small + 3);
+  const size_t npx = static_cast<size_t>(W) * H;
+  if (dbg && dbg->topk_src && topk) {
+    int32_t* tk;
+    PSM_TRY(ensure(ctx, ctx->topk_dbg, npx * k_sel, &tk));
+    bp.topk_dbg = tk;
+  }
+  const bool full_list = !topk && feat_dims > 0;
+  int cap = 0;
+  if (full_list) {
+    cap = 128;
+    uint2* lists;
+    PSM_TRY(ensure(ctx, ctx->lists, npx * cap, &lists));
+    bp.lists = lists;
+    bp.list_cap = cap;
+  }
+  launch_blend(bp, tiles, topk, st);
+  PSM_CUDA_TRY(cudaGetLastError());
+  if (full_list) {
+    int32_t ovf = 0;
+    PSM_CUDA_TRY(cudaMemcpyAsync(&ovf, small + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+    if (ovf > cap) {  // a pixel had more contributors than the list holds: re-run with room for all
+      cap = ovf;
+      uint2* lists;
+      PSM_TRY(ensure(ctx, ctx->lists, npx * cap, &lists));
+      bp.lists = lists;
+      bp.list_cap = cap;
+      PSM_CUDA_TRY(cudaMemsetAsync(small + 2, 0, 2 * sizeof(unsigned long long), st));
+      launch_blend(bp, tiles, topk, st);
+      PSM_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  record(ctx, 6);
+
+  // counters
+  PSM_CUDA_TRY(cudaMemcpyAsync(ctx->h_small, small, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  ctx->last.rn_total = static_cast<uint64_t>(rn);
+  ctx->last.n_proj = n_proj;
+  ctx->last.tiles_x = tiles_x;
+  ctx->last.tiles_y = tiles_y;
+
+  if (dbg) {
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+    if (dbg->tile_ranges) PSM_CUDA_TRY(cudaMemcpy(dbg->tile_ranges, ranges, sizeof(int32_t) * 2 * tiles, cudaMemcpyDeviceToHost));
+    const int64_t kcopy = rn < dbg->cap_keys ? rn : dbg->cap_keys;
+    if (kcopy > 0 && dbg->tile_vals) PSM_CUDA_TRY(cudaMemcpy(dbg->tile_vals, tvals_s, sizeof(int32_t) * kcopy, cudaMemcpyDeviceToHost));
+    if (kcopy > 0 && dbg->tile_keys) {
+      int32_t* rank_of;
+      uint64_t* dk;
+      PSM_TRY(ensure(ctx, ctx->rank_of, n, &rank_of));
+      PSM_TRY(ensure(ctx, ctx->dbg_keys, rn, &dk));
+      launch_rank_of(src_s, n_proj, rank_of, st);
+      launch_debug_keys(tkeys_s, tvals_s, rank_of, rn, dk, st);
+      PSM_CUDA_TRY(cudaGetLastError());
+      PSM_CUDA_TRY(cudaMemcpyAsync(dbg->tile_keys, dk, sizeof(uint64_t) * kcopy, cudaMemcpyDeviceToHost, st));
+    }
+    const int64_t pcopy = n_proj < dbg->cap_proj ? n_proj : dbg->cap_proj;
+    if (pcopy > 0 && dbg->depth_order)
+      PSM_CUDA_TRY(cudaMemcpyAsync(dbg->depth_order, src_s, sizeof(int32_t) * pcopy, cudaMemcpyDeviceToHost, st));
+    if (bp.topk_dbg)
+      PSM_CUDA_TRY(cudaMemcpyAsync(dbg->topk_src, bp.topk_dbg, sizeof(int32_t) * npx * k_sel, cudaMemcpyDeviceToHost, st));
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return PSM_OK;
+}
+
+void finish_counters(psm_ctx* ctx) {
+  const unsigned long long* h = reinterpret_cast<const unsigned long long*>(ctx->h_small);
+  ctx->last.nonempty_tiles = static_cast<int64_t>(h[1]);
+  ctx->last.blended_total = h[2];
+  ctx->last.rn_per_tile = h[1] > 0 ? static_cast<double>(ctx->last.rn_total) / static_cast<double>(h[1]) : 0.0;
+}
+
+void read_times(psm_ctx* ctx) {
+  if (!ctx->profiling) return;
+  float t[6] = {};
+  for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&t[i], ctx->ev[i], ctx->ev[i + 1]);
+  ctx->times.preprocess = t[0];
+  ctx->times.depth_sort = t[1];
+  ctx->times.emit = t[2];
+  ctx->times.tile_sort = t[3];
+  ctx->times.ranges = t[4];
+  ctx->times.blend = t[5];
+  cudaEventElapsedTime(&ctx->times.total, ctx->ev[0], ctx->ev[6]);
+}
+
+int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
+                  const psm_targets* tg, psm_counters* counters, psm_debug* dbg) {
+  if (!ctx || !sc || !cam || !cfg || !tg) return fail(ctx, PSM_EINVAL, "null argument");
+  if (cam->width <= 0 || cam->height <= 0) return fail(ctx, PSM_EINVAL, "camera: image size must be positive");
+  PSM_TRY(check_config(ctx, cfg, sc->c_sem + sc->n_q));
+  PSM_CUDA_TRY(cudaSetDevice(ctx->device));
+  const size_t npx = static_cast<size_t>(cam->width) * cam->height;
+  Planes pl;
+  // device planes: caller's when on_device and non-NULL, else context scratch
+  auto pick = [&](void* user, psm::Buf& b, size_t count, size_t elem, void** out) -> int {
+    if (tg->on_device && user) {
+      *out = user;
+      return PSM_OK;
+    }
+    char* p;
+    PSM_TRY(ensure(ctx, b, count * elem, &p));
+    *out = p;
+    return PSM_OK;
+  };
+  const int cs = sc->c_sem, nq = sc->n_q;
+  PSM_TRY(pick(tg->color, ctx->plane_color, npx * 3, 4, reinterpret_cast<void**>(&pl.color)));
+  PSM_TRY(pick(tg->depth, ctx->plane_depth, npx * 2, 4, reinterpret_cast<void**>(&pl.depth)));
+  PSM_TRY(pick(tg->normal, ctx->plane_normal, npx * 3, 4, reinterpret_cast<void**>(&pl.normal)));
+  PSM_TRY(pick(tg->alpha_acc, ctx->plane_alpha, npx, 4, reinterpret_cast<void**>(&pl.alpha)));
+  PSM_TRY(pick(tg->ins_argmax, ctx->plane_arg, npx, 4, reinterpret_cast<void**>(&pl.arg)));
+  PSM_TRY(pick(tg->blend_count, ctx->plane_cnt, npx, 4, reinterpret_cast<void**>(&pl.cnt)));
+  pl.sem = nullptr;
+  pl.ins = nullptr;
+  if (cs > 0 && (tg->sem_feat || !tg->on_device)) PSM_TRY(pick(tg->sem_feat, ctx->plane_sem, npx * cs, 4, reinterpret_cast<void**>(&pl.sem)));
+  if (nq > 0 && (tg->ins_dist || !tg->on_device)) PSM_TRY(pick(tg->ins_dist, ctx->plane_ins, npx * nq, 4, reinterpret_cast<void**>(&pl.ins)));
+  if (!tg->on_device) {
+    if (!tg->sem_feat) pl.sem = nullptr;
+    if (!tg->ins_dist) pl.ins = nullptr;
+  }
+  PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg));
+  if (!tg->on_device) {
+    cudaStream_t st = ctx->stream;
+    auto d2h = [&](void* dst, const void* src, size_t bytes) -> int {
+      if (dst) PSM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+      return PSM_OK;
+    };
+    PSM_TRY(d2h(tg->color, pl.color, npx * 12));
+    PSM_TRY(d2h(tg->depth, pl.depth, npx * 8));
+    PSM_TRY(d2h(tg->normal, pl.normal, npx * 12));
+    PSM_TRY(d2h(tg->alpha_acc, pl.alpha, npx * 4));
+    PSM_TRY(d2h(tg->ins_argmax, pl.arg, npx * 4));
+    PSM_TRY(d2h(tg->blend_count, pl.cnt, npx * 4));
+    if (pl.sem) PSM_TRY(d2h(tg->sem_feat, pl.sem, npx * cs * 4));
+    if (pl.ins) PSM_TRY(d2h(tg->ins_dist, pl.ins, npx * nq * 4));
+  }
+  if (counters || !tg->on_device || ctx->profiling) {
+    PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    finish_counters(ctx);
+    read_times(ctx);
+    if (counters) *counters = ctx->last;
+  }
+  return PSM_OK;
+}
+
+}  // namespace
+}  // namespace psm
+
+using psm::fail;
+
+extern "C" {
+
+int psm_create(int device, void* stream, psm_ctx** out) {
+  if (!out) return PSM_EINVAL;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0) {
+    cudaGetLastError();
+    return PSM_ECUDA;  // no CPU fallback
+  }
+  if (device < 0 || device >= count) return PSM_EINVAL;
+  psm_ctx* ctx = new psm_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) { delete ctx; return PSM_ECUDA; }
+  if (stream) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return PSM_ECUDA; }
+    ctx->own_stream = true;
+  }
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  if (cudaMallocHost(&ctx->h_small, 8 * sizeof(int64_t)) != cudaSuccess) { delete ctx; return PSM_ENOMEM; }
+  std::memset(ctx->h_small, 0, 8 * sizeof(int64_t));
+  *out = ctx;
+  return PSM_OK;
+}
+
+int psm_destroy(psm_ctx* ctx) {
+  if (!ctx) return PSM_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->depth_bits, &ctx->tile_cnt, &ctx->valid, &ctx->pos,
+                      &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s, &ctx->cnt_rank, &ctx->off_rank,
+                      &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->cub_tmp,
+                      &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,
+                      &ctx->plane_color, &ctx->plane_depth, &ctx->plane_normal, &ctx->plane_sem, &ctx->plane_ins,
+                      &ctx->plane_arg, &ctx->plane_alpha, &ctx->plane_cnt};
+  for (psm::Buf* b : bufs) psm::free_buf(*b);
+  for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+  if (ctx->h_small) cudaFreeHost(ctx->h_small);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return PSM_OK;
+}
+
+const char* psm_last_error(const psm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int psm_set_profiling(psm_ctx* ctx, int enabled) {
+  if (!ctx) return PSM_EINVAL;
+  ctx->profiling = enabled != 0;
+  return PSM_OK;
+}
+
+int psm_get_stage_times(const psm_ctx* ctx, psm_stage_times* out) {
+  if (!ctx || !out) return PSM_EINVAL;
+  *out = ctx->times;
+  return PSM_OK;
+}
+
+int psm_sync(psm_ctx* ctx) {
+  if (!ctx) return PSM_EINVAL;
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return psm::fail_cuda(ctx, e, "cudaStreamSynchronize", __FILE__, __LINE__);
+  psm::finish_counters(ctx);
+  psm::read_times(ctx);
+  return PSM_OK;
+}
+
+int psm_last_counters(const psm_ctx* ctx, psm_counters* out) {
+  if (!ctx || !out) return PSM_EINVAL;
+  *out = ctx->last;
+  return PSM_OK;
+}
+
+int psm_scene_upload(psm_ctx* ctx, const double* surfels13, int64_t n, const double* f_sem, int32_t c_sem,
+                     const double* labels, int32_t n_q, psm_scene** out) {
+  if (!ctx || !out) return PSM_EINVAL;
+  *out = nullptr;
+  if (n < 0 || n > 0x7fffffffLL || c_sem < 0 || n_q < 0) return fail(ctx, PSM_EINVAL, "scene: bad sizes");
+  if (n > 0 && !surfels13) return fail(ctx, PSM_EINVAL, "scene: null surfels");
+  if (c_sem > 0 && n > 0 && !f_sem) return fail(ctx, PSM_EINVAL, "scene: null f_sem with c_sem > 0");
+  if (!labels) n_q = 0;
+  if (n == 0) c_sem = 0;  // SceneMap::c_sem() of an empty scene (core_types.hpp:108)
+  PSM_CUDA_TRY(cudaSetDevice(ctx->device));
+  psm_scene* sc = new psm_scene();
+  sc->device = ctx->device;
+  sc->n = n;
+  sc->c_sem = c_sem;
+  sc->n_q = n_q;
+  const int D = c_sem + n_q;
+  if (n > 0) {
+    cudaError_t e = cudaMalloc(&sc->surfels, sizeof(double) * 13 * n);
+    if (e == cudaSuccess) e = cudaMemcpy(sc->surfels, surfels13, sizeof(double) * 13 * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && D > 0) {
+      std::vector<float> f(static_cast<size_t>(n) * D);
+      for (int64_t i = 0; i < n; ++i) {
+        for (int c = 0; c < c_sem; ++c) f[i * D + c] = static_cast<float>(f_sem[i * c_sem + c]);
+        for (int q = 0; q < n_q; ++q) f[i * D + c_sem + q] = static_cast<float>(labels[i * n_q + q]);
+      }
+      e = cudaMalloc(&sc->feat, sizeof(float) * f.size());
+      if (e == cudaSuccess) e = cudaMemcpy(sc->feat, f.data(), sizeof(float) * f.size(), cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) {
+      psm_scene_free(ctx, sc);
+      return psm::fail_cuda(ctx, e, "scene upload", __FILE__, __LINE__);
+    }
+  }
+  *out = sc;
+  return PSM_OK;
+}
+
+int psm_scene_free(psm_ctx* ctx, psm_scene* sc) {
+  (void)ctx;
+  if (!sc) return PSM_OK;
+  cudaSetDevice(sc->device);
+  if (sc->surfels) cudaFree(sc->surfels);
+  if (sc->feat) cudaFree(sc->feat);
+  delete sc;
+  return PSM_OK;
+}
+
+int psm_scene_info(const psm_scene* sc, int64_t* n, int32_t* c_sem, int32_t* n_q) {
+  if (!sc) return PSM_EINVAL;
+  if (n) *n = sc->n;
+  if (c_sem) *c_sem = sc->c_sem;
+  if (n_q) *n_q = sc->n_q;
+  return PSM_OK;
+}
+
+int psm_render(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam, const psm_raster_config* cfg,
+               const psm_targets* targets, psm_counters* counters) {
+  return psm::render_common(ctx, scene, cam, cfg, targets, counters, nullptr);
+}
+
+int psm_render_debug(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam, const psm_raster_config* cfg,
+                     const psm_targets* targets, psm_counters* counters, psm_debug* debug) {
+  return psm::render_common(ctx, scene, cam, cfg, targets, counters, debug);
+}
+
+int psm_render_batch(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cams, int32_t n_views,
+                     const psm_raster_config* cfg, const psm_targets* targets, psm_counters* counters) {
+  if (!ctx || !cams || !targets || n_views < 0) return PSM_EINVAL;
+  for (int32_t v = 0; v < n_views; ++v) {
+    const int st = psm_render(ctx, scene, cams + v, cfg, targets + v, counters ? counters + v : nullptr);
+    if (st != PSM_OK) return st;
+  }
+  return PSM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// psm_kernels.h — launcher declarations of the render pipeline (K1..K7).
+#ifndef PSM_KERNELS_H
+#define PSM_KERNELS_H
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "psm_device.cuh"
+
+namespace psm {
+
+struct BlendParams {
+  const int32_t* ranges;  // [tiles][2]
+  const uint32_t* vals;   // tile-sorted source ids
+  const SurfRec* recs;
+  const float* feat;      // [N][feat_dims]: f_sem | labels, fp32
+  int32_t feat_dims, c_sem, n_q;
+  int32_t width, height, tiles_x;
+  double cam_cx, cam_cy, cam_fx, cam_fy;
+  double chi2, alpha_min, t_min, bg0, bg1, bg2;
+  int32_t support_cutoff, render_depth_normal, k_sel;
+  float *color, *depth, *normal, *sem_feat, *ins_dist, *alpha_acc;
+  int32_t *ins_argmax, *blend_count;
+  unsigned long long* blended_total;
+  int32_t* topk_dbg;      // optional [W*H*k_sel]
+  uint2* lists;           // full blending with features: [W*H][list_cap]
+  int32_t list_cap;
+  int32_t* list_overflow;
+};
+
+// K1 preprocess.cu
+void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
+                       BinRec* bins, uint64_t* depth_bits, int32_t* tile_cnt, int32_t* valid, int32_t* err,
+                       cudaStream_t stream);
+
+// binning.cu
+void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n,
+                    uint64_t* keys_out, uint32_t* src_out, cudaStream_t st);
+void launch_gather_counts(const uint32_t* src_by_rank, const int32_t* tile_cnt, int64_t n_proj, uint32_t* cnt_by_rank,
+                          cudaStream_t st);
+void launch_emit(const uint32_t* src_by_rank, const uint32_t* offsets, int64_t n_proj, const SurfRec* recs,
+                 const BinRec* bins, const DevRaster& rs, int img_h, uint32_t* tile_keys, uint32_t* tile_vals,
+                 cudaStream_t st);
+void launch_ranges(const uint32_t* sorted_tiles, int64_t rn, int32_t* ranges, unsigned long long* nonempty,
+                   cudaStream_t st);
+void launch_rank_of(const uint32_t* src_by_rank, int64_t n_proj, int32_t* rank_of, cudaStream_t st);
+void launch_debug_keys(const uint32_t* sorted_tiles, const uint32_t* sorted_vals, const int32_t* rank_of, int64_t rn,
+                       uint64_t* keys_out, cudaStream_t st);
+
+// blend.cu
+int blend_kmax_for(int k_sel);
+int blend_nch_for(int feat_dims);
+void launch_blend(const BlendParams& p, int tiles, bool topk, cudaStream_t st);
+
+}  // namespace psm
+
+#endif  // PSM_KERNELS_H

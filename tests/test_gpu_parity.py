@@ -1,0 +1,223 @@
+"""GPU parity: the sm_100a path (through the C-ABI, libpsm.so) against the CPU oracle on the same
+seeded inputs. Bit-exact: sorted (tile, depth-rank) keys, tile lists, per-tile ranges, depth order,
+Top-K source sets, blend counts, RN-Total / blended_total / n_proj. Within 1e-4 absolute (the
+north-star tolerance): colour, depth, normal, alpha, semantic-feature and label planes."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from paper_2604_10982_b200 import (Binning, Blending, RasterConfig, Renderer, RenderTargets, SceneMap, StreetSpec,
+                                   density_scale, make_street_scene)
+from paper_2604_10982_b200 import _abi as A
+from tests.helpers import Rng, facing_surfel, front_camera, scene_of
+
+pytestmark = pytest.mark.gpu
+ATOL = 1e-4  # north-star tolerance for fp32 planes
+
+
+@pytest.fixture(scope="module")
+def rend():
+    r = Renderer(0)
+    yield r
+    r.close()
+
+
+def gpu_render(rend, scene, labels, cam, cfg, debug=True):
+    out = RenderTargets()
+    dbg = None
+    arrs = {}
+    if debug:
+        ref = O.render(scene, labels, cam, cfg, planes=False)  # sizes for the debug buffers
+        rn, n_proj = ref["counters"]["rn_total"], ref["counters"]["n_proj"]
+        tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+        k = max(cfg.top_k, 1)
+        arrs = {"tile_keys": np.zeros(max(rn, 1), np.uint64), "tile_vals": np.zeros(max(rn, 1), np.int32),
+                "tile_ranges": np.zeros((tiles, 2), np.int32), "depth_order": np.zeros(max(n_proj, 1), np.int32),
+                "topk_src": np.full((cam.height, cam.width, k), -1, np.int32)}
+        p = lambda a: a.ctypes.data_as(C.c_void_p)
+        dbg = A.psm_debug(p(arrs["tile_keys"]), p(arrs["tile_vals"]), rn, p(arrs["tile_ranges"]),
+                          p(arrs["depth_order"]), n_proj, p(arrs["topk_src"]))
+    rend.render_into(out, scene, labels, cam, cfg, debug=dbg)
+    if debug:
+        arrs["tile_keys"] = arrs["tile_keys"][:out.rn_total]
+        arrs["tile_vals"] = arrs["tile_vals"][:out.rn_total]
+        arrs["depth_order"] = arrs["depth_order"][:out.n_proj]
+    return out, arrs
+
+
+def assert_parity(rend, scene, labels, cam, cfg, check_debug=True):
+    g, gd = gpu_render(rend, scene, labels, cam, cfg, debug=check_debug)
+    o = O.render(scene, labels, cam, cfg, debug=check_debug)
+    oc = o["counters"]
+    # counters (raster.hpp:36-37,65)
+    assert g.rn_total == oc["rn_total"]
+    assert g.n_proj == oc["n_proj"]
+    assert g.blended_total == oc["blended_total"]
+    assert g.rn_per_tile == pytest.approx(oc["rn_per_tile"], rel=0, abs=0)
+    if check_debug:
+        assert np.array_equal(gd["depth_order"], o["depth_order"]), "depth order"
+        assert np.array_equal(gd["tile_ranges"], o["tile_ranges"]), "tile ranges"
+        assert np.array_equal(gd["tile_vals"], o["tile_vals"]), "tile lists"
+        assert np.array_equal(gd["tile_keys"], o["tile_keys"]), "sorted keys"
+        if cfg.blending == Blending.TopK:
+            gs = np.sort(np.where(gd["topk_src"] < 0, np.iinfo(np.int32).max, gd["topk_src"]), axis=-1)
+            os_ = np.sort(np.where(o["topk_src"] < 0, np.iinfo(np.int32).max, o["topk_src"]), axis=-1)
+            assert np.array_equal(gs, os_), "Top-K source sets"
+    assert np.array_equal(g.blend_count, o["blend_count"]), "blend_count"
+    for k in ("color", "depth", "normal", "alpha_acc", "sem_feat", "ins_dist"):
+        a, b = getattr(g, k), o[k]
+        assert a.shape == b.shape, k
+        if a.size:
+            err = np.max(np.abs(a.astype(np.float64) - b))
+            assert err <= ATOL, (k, err)
+    # ins_argmax: exact except where the oracle's top-2 label masses tie within fp32 accumulation noise
+    ga, oa = g.ins_argmax[..., 0], o["ins_argmax"][..., 0]
+    if o["ins_dist"].shape[-1] > 1:
+        srt = np.sort(o["ins_dist"], axis=-1)
+        near_tie = (srt[..., -1] - srt[..., -2]) < 1e-5
+        assert np.all((ga == oa) | near_tie)
+    else:
+        assert np.array_equal(ga, oa)
+    return g, o
+
+
+# ------------------------------------------------------------ test_raster.cpp KATs through the GPU
+def test_gpu_single_opaque_surfel(rend):
+    cam = front_camera()
+    sc = scene_of([facing_surfel((0, 0, 2), 0.2, 0.2, 1.0, (0.3, 0.6, 0.9))])
+    g, _ = assert_parity(rend, sc, None, cam, RasterConfig(background=(0.1, 0.1, 0.1)))
+    x, y = int(cam.cx), int(cam.cy)
+    assert np.allclose(g.color[y, x], (0.3, 0.6, 0.9), atol=1e-6)
+    assert abs(g.alpha_acc[y, x, 0] - 1.0) < 1e-6
+    assert abs(g.depth[y, x, 0] - 2.0) < 1e-5 and abs(g.depth[y, x, 1] - 2.0) < 1e-5
+
+
+def test_gpu_two_surfel_alpha_arithmetic(rend):
+    cam = front_camera()
+    sc = scene_of([facing_surfel((0, 0, 2), 0.2, 0.2, 0.5, (1, 0, 0)),
+                   facing_surfel((0, 0, 3), 0.3, 0.3, 1.0, (0, 1, 0))])
+    g, _ = assert_parity(rend, sc, None, cam, RasterConfig())
+    x, y = int(cam.cx), int(cam.cy)
+    assert np.allclose(g.color[y, x], (0.5, 0.5, 0.0), atol=1e-6)
+
+
+def test_gpu_empty_scene(rend):
+    cam = front_camera(16, 16)
+    g = rend.render(SceneMap(np.zeros((0, 13))), None, cam, RasterConfig(background=(0.25, 0.5, 0.75)))
+    assert np.all(g.color == np.array([0.25, 0.5, 0.75], np.float32))
+    assert np.all(g.alpha_acc == 0) and np.all(g.ins_argmax == -1) and np.all(g.blend_count == 0)
+    assert g.blended_total == 0 and g.rn_total == 0
+
+
+def test_gpu_degenerate_quaternion_raises(rend):
+    cam = front_camera()
+    bad = facing_surfel((0, 0, 2), 0.2, 0.2, 1.0, (1, 1, 1), quat=(0, 0, 0, 0))
+    with pytest.raises(ValueError):
+        rend.render(scene_of([bad]), None, cam, RasterConfig())
+    # behind the camera the reference never reaches rotation_from_quat (raster.cpp:97-99)
+    behind = facing_surfel((0, 0, -2), 0.2, 0.2, 1.0, (1, 1, 1), quat=(0, 0, 0, 0))
+    rend.render(scene_of([behind]), None, cam, RasterConfig())
+
+
+# ------------------------------------------------------------ street scenes
+@pytest.fixture(scope="module")
+def c0():  # acceptance standard street (acceptance.cpp:33-42): 12k surfels, 256x192, C_sem 32, 256 labels
+    return make_street_scene(StreetSpec(n_surfels=12000, image_w=256, image_h=192, c_sem=32, seed=7))
+
+
+@pytest.mark.parametrize("binning", [Binning.Circle, Binning.Aabb, Binning.Ellipse])
+@pytest.mark.parametrize("blending", [Blending.Full, Blending.TopK])
+def test_gpu_c0_grid(rend, c0, binning, blending):
+    sc, labels, cam = c0
+    assert_parity(rend, sc, labels, cam, RasterConfig(binning=binning, blending=blending, top_k=16))
+
+
+def test_gpu_c1_rgb_depth(rend):
+    sc, _, cam = make_street_scene(StreetSpec(n_surfels=10000, image_w=256, image_h=256, c_sem=0))
+    assert_parity(rend, sc, None, cam, RasterConfig(binning=Binning.Aabb))
+
+
+@pytest.mark.parametrize("k", [1, 5, 8, 16, 32])
+def test_gpu_topk_sizes(rend, k):
+    sc, _, cam = make_street_scene(StreetSpec(n_surfels=3000, image_w=128, image_h=96, c_sem=64,
+                                              scale_mult=density_scale(3000, 128, 96)))
+    assert_parity(rend, sc, None, cam, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=k))
+
+
+@pytest.mark.parametrize("variant", ["no_cutoff", "no_depth_normal", "background", "t_min0", "ragged", "chi2"])
+def test_gpu_config_variants(rend, variant):
+    w, h = (100, 70) if variant == "ragged" else (96, 64)
+    sc, labels, cam = make_street_scene(StreetSpec(n_surfels=1500, image_w=w, image_h=h, c_sem=8, n_instances=12))
+    cfg = {
+        "no_cutoff": RasterConfig(support_cutoff=False, binning=Binning.Ellipse),  # Ellipse falls back to AABB
+        "no_depth_normal": RasterConfig(render_depth_normal=False, blending=Blending.TopK, top_k=4),
+        "background": RasterConfig(background=(0.2, 0.4, 0.6), binning=Binning.Circle),
+        "t_min0": RasterConfig(t_min=0.0, blending=Blending.TopK, top_k=8),
+        "ragged": RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=8),
+        "chi2": RasterConfig(chi2=4.0, binning=Binning.Ellipse),
+    }[variant]
+    assert_parity(rend, sc, labels, cam, cfg)
+
+
+def test_gpu_random_surfels(rend):
+    rng = Rng(17)
+    rows = []
+    for _ in range(600):
+        c = (rng.uniform(-1.2, 1.2), rng.uniform(-1, 1), rng.uniform(0.5, 6))
+        q = rng.unit_quaternion()
+        rows.append(facing_surfel(c, rng.uniform(0.01, 0.6), rng.uniform(0.01, 0.6), rng.uniform(0.05, 1.0),
+                                  (rng.uniform(), rng.uniform(), rng.uniform()), quat=q))
+    f = np.array([[rng.normal() for _ in range(40)] for _ in rows])
+    sc = SceneMap(np.array(rows), f)
+    cam = front_camera(160, 120, 120.0)
+    for cfg in (RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=8),
+                RasterConfig(binning=Binning.Circle, blending=Blending.Full)):
+        assert_parity(rend, sc, None, cam, cfg)
+
+
+def test_gpu_permutation_bit_identical(rend):
+    sc, labels, cam = make_street_scene(StreetSpec(n_surfels=2000, image_w=96, image_h=64, c_sem=3,
+                                                   n_instances=8))
+    perm = np.random.default_rng(3).permutation(len(sc))
+    sh = SceneMap(sc.surfels[perm], sc.f_sem[perm])
+    cfg = RasterConfig(blending=Blending.TopK, top_k=8)
+    a = rend.render(sc, labels, cam, cfg)
+    b = rend.render(sh, labels[perm], cam, cfg)
+    for k in ("color", "depth", "normal", "blend_count", "alpha_acc"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+# ------------------------------------------------------------ full-size C3 (the bench workload)
+@pytest.fixture(scope="module")
+def c3():
+    n, w, h = 1_000_000, 1280, 720
+    return make_street_scene(StreetSpec(n_surfels=n, image_w=w, image_h=h, c_sem=64,
+                                        scale_mult=density_scale(n, w, h)), with_labels=False)
+
+
+def test_gpu_c3_full_size_parity(rend, c3):
+    """1M surfels, 1280x720, 64-d features, Top-K = 8, Ellipse binning: every bit-exact artefact and
+    every plane against the oracle at the benchmark's own size."""
+    sc, _, cam = c3
+    g, o = assert_parity(rend, sc, None, cam, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK,
+                                                          top_k=8))
+    assert g.rn_total > 1_000_000
+
+
+def test_gpu_c3_binning_output_identity(rend, c3):
+    """Size-independent property at full size: Circle, AABB and Ellipse binning give bit-identical
+    planes (support cutoff on), RN-Total strictly decreasing."""
+    sc, _, cam = c3
+    outs = [rend.render(sc, None, cam, RasterConfig(binning=b, blending=Blending.TopK, top_k=8))
+            for b in (Binning.Circle, Binning.Aabb, Binning.Ellipse)]
+    for o in outs[1:]:
+        for k in ("color", "depth", "normal", "sem_feat", "blend_count", "alpha_acc"):
+            assert np.array_equal(getattr(outs[0], k), getattr(o, k)), k
+        assert o.blended_total == outs[0].blended_total
+    assert outs[0].rn_total > outs[1].rn_total > outs[2].rn_total
+    bc = outs[0].blend_count
+    assert outs[0].blended_total == int(np.minimum(bc, 8).sum())
+    assert np.all(outs[0].alpha_acc >= 0) and np.all(outs[0].alpha_acc <= 1)
