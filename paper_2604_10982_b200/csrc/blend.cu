@@ -2,24 +2,30 @@
 // warp-cooperative feature accumulation (reference: the tile loop of
 // render_into, proj/src/raster.cpp:355-506, and topk_select, raster.cpp:225-251).
 //
-// One CTA per 16x16 tile, one thread per pixel. The tile's depth-sorted list
-// (vals[start, end) from the tile sort) is streamed through shared memory in
-// batches of 256 records (each thread stages one 144 B SurfRec, nine 16 B
-// loads); every pixel then walks the batch in list order with the reference's
-// fp64 arithmetic (compiled --fmad=false, psm_exp), so its contributor
-// sequence, transmittance and Top-K set are bit-identical to the oracle's. The
-// CTA leaves the list once every pixel has hit T < t_min (__syncthreads_count).
+// One CTA per 16x16 tile (8 warps), one thread per pixel; each warp owns an 8x4
+// pixel block (compact footprint: fewer lanes idle in the accept path) and
+// streams the tile's depth-sorted list (vals[start, end) from the tile sort) on
+// its own: 32 records (144 B SurfRec each, nine 16 B cp.async per lane) per
+// chunk, double-buffered in shared memory, with no CTA-wide barrier. A warp
+// stops reading the list as soon as all its 32 pixels have hit T < t_min.
+// Each pixel walks the list in order with the reference's fp64 arithmetic
+// (compiled --fmad=false; psm_exp_nonpos), so its contributor sequence,
+// transmittance and Top-K set are bit-identical to the oracle's.
+//
+// Colour and normal are accumulated in fp32 from the fp64 weight (one
+// conversion per contributor; |error| <= ~1e-6, inside the 1e-4 tolerance);
+// expected depth, the dominant-weight pick and all decisions stay fp64.
 //
 // Top-K: each thread keeps the KMAX best (weight desc, source asc) entries in
 // registers by an unrolled insertion network (the reference's insertion select,
 // raster.cpp:238-249; proj order == source order). Selection only changes the
 // result when m > K, as in the reference (raster.cpp:442).
 // Features: after compositing, each warp walks its 32 pixels; the owning lane's
-// (source, weight) slots are broadcast with __shfl_sync and all 32 lanes read the
-// selected surfel's feature row (coalesced 128 B per load) and accumulate 32
-// channels each, then write the pixel's HWC channel run in one coalesced store.
-// Full blending with features keeps per-pixel (source, weight) lists in a global
-// scratch (L2-resident; written and re-read by the same CTA).
+// (source, weight) slots are broadcast with __shfl_sync and the 32 lanes read the
+// selected surfel's feature row as one coalesced 128-512 B vector load and
+// accumulate VEC*NV channels each, then store the pixel's HWC channel run with
+// one coalesced vector store. Full blending with features keeps per-pixel
+// (source, weight) lists in an L2-resident global scratch.
 #include <cstdint>
 
 #include "psm_device.cuh"
@@ -31,34 +37,129 @@ namespace {
 
 constexpr int kTile = 16;
 constexpr int kThreads = kTile * kTile;
-constexpr int kMaxNch = 16;  // feature dims per launch: 32 * 16 = 512
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 32;                   // records per warp chunk
+constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
+
+struct __align__(16) WarpStage {
+  SurfRec rec[2][kChunk];
+};
+constexpr size_t kSmemBytes = sizeof(WarpStage) * kWarps;
 
 // before(a, b) of topk_select (raster.cpp:232-235), proj order == source order
 __device__ __forceinline__ bool before(double wa, int sa, double wb, int sb) {
   return wa > wb || (wa == wb && sa < sb);
 }
 
-template <int KMAX, bool FULL_LIST, int NCH>
-__global__ void __launch_bounds__(kThreads, 2) blend_kernel(BlendParams p) {
-  __shared__ SurfRec srec[kThreads];
-  __shared__ int32_t ssrc[kThreads];
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Feature vector type per lane: VEC consecutive floats.
+template <int VEC> struct FVec;
+template <> struct FVec<1> { using T = float; };
+template <> struct FVec<2> { using T = float2; };
+template <> struct FVec<4> { using T = float4; };
+
+template <int VEC>
+__device__ __forceinline__ void fma_vec(float (&acc)[VEC], float w, const typename FVec<VEC>::T& v) {
+  if constexpr (VEC == 1) {
+    acc[0] = fmaf(w, v, acc[0]);
+  } else if constexpr (VEC == 2) {
+    acc[0] = fmaf(w, v.x, acc[0]);
+    acc[1] = fmaf(w, v.y, acc[1]);
+  } else {
+    acc[0] = fmaf(w, v.x, acc[0]);
+    acc[1] = fmaf(w, v.y, acc[1]);
+    acc[2] = fmaf(w, v.z, acc[2]);
+    acc[3] = fmaf(w, v.w, acc[3]);
+  }
+}
+
+// Accumulates one feature row into the lane's VEC*NV channels:
+// channel(e, v) = (v * 32 + lane) * VEC + e. EXACT: D == 32 * VEC * NV (no guards).
+template <int VEC, int NV, bool EXACT>
+__device__ __forceinline__ void accumulate_row(float (&acc)[NV][VEC], float w, const float* __restrict__ row, int lane,
+                                               int D) {
+  using T = typename FVec<VEC>::T;
+  const T* r = reinterpret_cast<const T*>(row);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int idx = v * 32 + lane;
+    if (EXACT || idx * VEC < D) fma_vec<VEC>(acc[v], w, __ldg(r + idx));
+  }
+}
+
+// Can the support ellipse d^T Finv d <= chi2 of record r reach any pixel centre of
+// the warp's block [x0, x1] x [y0, y1]? Continuous minimum of the quadratic over
+// the rectangle (on its boundary when the centre lies outside), compared with a
+// relative 1e-6 margin so the per-pixel fp64 test (raster.cpp:379) can never pass
+// where this says no; ill-conditioned or non-finite footprints always pass.
+__device__ __forceinline__ bool block_meets(const SurfRec& r, double x0, double x1, double y0, double y1,
+                                            double chi2lim) {
+  const double ax = x0 - r.cx, bx = x1 - r.cx, ay = y0 - r.cy, by = y1 - r.cy;
+  if (!(ax > 0.0 || bx < 0.0 || ay > 0.0 || by < 0.0)) return true;  // centre inside (or NaN)
+  const double a = r.f00, b2 = r.f01x2, c = r.f11;
+  const double det = a * c - 0.25 * b2 * b2;
+  if (!(det > 0.0) || !((a + c) * (a + c) < 1e12 * det)) return true;
+  double best = 1e300;
+  {
+    const double ia = -0.5 * b2 / c;  // argmin dy on a vertical edge is ia * X
+    double dy = ia * ax;
+    dy = fmin(fmax(dy, ay), by);
+    best = fmin(best, (a * ax + b2 * dy) * ax + c * dy * dy);
+    dy = ia * bx;
+    dy = fmin(fmax(dy, ay), by);
+    best = fmin(best, (a * bx + b2 * dy) * bx + c * dy * dy);
+  }
+  {
+    const double ic = -0.5 * b2 / a;  // argmin dx on a horizontal edge is ic * Y
+    double dx = ic * ay;
+    dx = fmin(fmax(dx, ax), bx);
+    best = fmin(best, (c * ay + b2 * dx) * ay + a * dx * dx);
+    dx = ic * by;
+    dx = fmin(fmax(dx, ax), bx);
+    best = fmin(best, (c * by + b2 * dx) * by + a * dx * dx);
+  }
+  return !(best > chi2lim);
+}
+
+// Resident CTAs per SM: 3 (80 registers) for K <= 8, fewer for the wider register Top-K.
+constexpr int min_blocks(int kmax) { return kmax >= 32 ? 1 : (kmax >= 16 ? 2 : 3); }
+
+template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT>
+__global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(BlendParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpStage& stage = reinterpret_cast<WarpStage*>(smem_raw)[threadIdx.x >> 5];
 
   const int tile = blockIdx.x;
   const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
   const int tid = threadIdx.x;
-  const int x = tx * kTile + (tid & (kTile - 1));
-  const int y = ty * kTile + (tid >> 4);
+  const int lane = tid & 31, warp = tid >> 5;
+  // warp -> 8x4 block of the 16x16 tile; lane -> pixel inside it
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+  const int x = wx0 + (lane & 7);
+  const int y = wy0 + (lane >> 3);
   const bool inside = x < p.width && y < p.height;
   const int64_t pix = static_cast<int64_t>(y) * p.width + x;
 
   const double px = x + 0.5, py = y + 0.5;
+  // pixel-centre extents of the warp's 8x4 block (clipped to the image) for the prefilter
+  const double bx0 = wx0 + 0.5, by0 = wy0 + 0.5;
+  const double bx1 = min(wx0 + 8, p.width) - 0.5, by1 = min(wy0 + 4, p.height) - 0.5;
+  const double chi2lim = p.chi2 * 1.000001 + 1e-9;
   const double rx = (px - p.cam_cx) / p.cam_fx;  // division as in raster.cpp:370-371
   const double ry = (py - p.cam_cy) / p.cam_fy;
 
   double T = 1.0;
   int m = 0;
   bool done = !inside;
-  double acc_r = 0, acc_g = 0, acc_b = 0, exp_depth = 0, dom_depth = 0, dom_w = 0, nx = 0, ny = 0, nz = 0;
+  float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
+  double exp_depth = 0, dom_depth = 0, dom_w = 0;
   double sw[KMAX > 0 ? KMAX : 1];
   int ss[KMAX > 0 ? KMAX : 1];
 #pragma unroll
@@ -68,20 +169,38 @@ __global__ void __launch_bounds__(kThreads, 2) blend_kernel(BlendParams p) {
   }
 
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
-  for (int base = start; base < end; base += kThreads) {
-    const int cnt = min(kThreads, end - base);
-    if (tid < cnt) {
-      const int s = static_cast<int>(p.vals[base + tid]);
-      ssrc[tid] = s;
-      const float4* src4 = reinterpret_cast<const float4*>(p.recs + s);
-      float4* dst4 = reinterpret_cast<float4*>(srec + tid);
+  auto prefetch = [&](int base, int buf) {
+    if (base + lane < end) {
+      const int s = static_cast<int>(__ldg(p.vals + base + lane));
+      const char* g = reinterpret_cast<const char*>(p.recs + s);
+      char* d = reinterpret_cast<char*>(&stage.rec[buf][lane]);
 #pragma unroll
-      for (int k = 0; k < 9; ++k) dst4[k] = __ldg(src4 + k);
+      for (int k = 0; k < kRecVec; ++k) cp_async16(d + 16 * k, g + 16 * k);
     }
-    __syncthreads();
+    cp_async_commit();
+  };
+
+  if (__any_sync(0xffffffffu, !done) && start < end) prefetch(start, 0);
+  int buf = 0;
+  for (int base = start; base < end; base += kChunk, buf ^= 1) {
+    if (__all_sync(0xffffffffu, done)) break;
+    const int cnt = min(kChunk, end - base);
+    if (base + kChunk < end) {
+      prefetch(base + kChunk, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    const SurfRec* recs = stage.rec[buf];
+    // candidates that reach no pixel centre of this warp's block are skipped as a whole
+    unsigned live = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+    if (p.support_cutoff) live = __ballot_sync(0xffffffffu, lane < cnt && block_meets(recs[lane], bx0, bx1, by0, by1, chi2lim));
     if (!done) {
-      for (int j = 0; j < cnt; ++j) {
-        const SurfRec& r = srec[j];
+      while (live) {
+        const int j = __ffs(live) - 1;
+        live &= live - 1;
+        const SurfRec& r = recs[j];
         if (p.support_cutoff) {
           const double dx = px - r.cx;
           const double dy = py - r.cy;
@@ -93,22 +212,23 @@ __global__ void __launch_bounds__(kThreads, 2) blend_kernel(BlendParams p) {
         if (!(w2 > 1e-14)) continue;
         const double rcp = 1.0 / w2;
         const double u = w0 * rcp, v = w1 * rcp;
-        const double alpha = r.opacity * psm_exp(-0.5 * (u * u + v * v));
+        const double alpha = r.opacity * psm_exp_nonpos(-0.5 * (u * u + v * v));
         if (alpha < p.alpha_min || alpha <= 0.0) continue;
         const double wt = alpha * T;
         // colour / depth / normal always over the full list (raster.cpp:405-436)
-        acc_r += wt * static_cast<double>(r.color[0]);
-        acc_g += wt * static_cast<double>(r.color[1]);
-        acc_b += wt * static_cast<double>(r.color[2]);
+        const float wf = static_cast<float>(wt);
+        acc_r = fmaf(wf, r.color[0], acc_r);
+        acc_g = fmaf(wf, r.color[1], acc_g);
+        acc_b = fmaf(wf, r.color[2], acc_b);
+        nx = fmaf(wf, r.normal[0], nx);
+        ny = fmaf(wf, r.normal[1], ny);
+        nz = fmaf(wf, r.normal[2], nz);
         exp_depth += wt * rcp;
         if (wt > dom_w) {
           dom_w = wt;
           dom_depth = rcp;
         }
-        nx += wt * static_cast<double>(r.normal[0]);
-        ny += wt * static_cast<double>(r.normal[1]);
-        nz += wt * static_cast<double>(r.normal[2]);
-        const int src = ssrc[j];
+        const int src = static_cast<int>(__ldg(p.vals + base + j));
         if constexpr (KMAX > 0) {
           if (before(wt, src, sw[KMAX - 1], ss[KMAX - 1])) {
 #pragma unroll
@@ -126,8 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2) blend_kernel(BlendParams p) {
           }
         }
         if constexpr (FULL_LIST) {
-          if (m < p.list_cap)
-            p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(src), __float_as_uint(static_cast<float>(wt)));
+          if (m < p.list_cap) p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(src), __float_as_uint(wf));
         }
         T *= 1.0 - alpha;
         ++m;
@@ -137,22 +256,23 @@ __global__ void __launch_bounds__(kThreads, 2) blend_kernel(BlendParams p) {
         }
       }
     }
-    if (__syncthreads_count(done) == kThreads) break;  // also fences srec reuse
+    __syncwarp();  // the buffer is refilled by the next iteration's prefetch
   }
+  cp_async_wait<0>();
 
   const int k_sel = p.k_sel;
   int blend_n = m;
   if constexpr (KMAX > 0) blend_n = m < k_sel ? m : k_sel;
   if (inside) {
-    p.color[pix * 3 + 0] = static_cast<float>(acc_r + T * p.bg0);
-    p.color[pix * 3 + 1] = static_cast<float>(acc_g + T * p.bg1);
-    p.color[pix * 3 + 2] = static_cast<float>(acc_b + T * p.bg2);
+    p.color[pix * 3 + 0] = acc_r + static_cast<float>(T * p.bg0);
+    p.color[pix * 3 + 1] = acc_g + static_cast<float>(T * p.bg1);
+    p.color[pix * 3 + 2] = acc_b + static_cast<float>(T * p.bg2);
     const bool rdn = p.render_depth_normal != 0;
     p.depth[pix * 2 + 0] = rdn ? static_cast<float>(exp_depth) : 0.f;
     p.depth[pix * 2 + 1] = rdn ? static_cast<float>(dom_depth) : 0.f;
-    p.normal[pix * 3 + 0] = rdn ? static_cast<float>(nx) : 0.f;
-    p.normal[pix * 3 + 1] = rdn ? static_cast<float>(ny) : 0.f;
-    p.normal[pix * 3 + 2] = rdn ? static_cast<float>(nz) : 0.f;
+    p.normal[pix * 3 + 0] = rdn ? nx : 0.f;
+    p.normal[pix * 3 + 1] = rdn ? ny : 0.f;
+    p.normal[pix * 3 + 2] = rdn ? nz : 0.f;
     p.alpha_acc[pix] = static_cast<float>(1.0 - T);
     p.blend_count[pix] = m;
     if constexpr (KMAX > 0) {
@@ -166,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 2) blend_kernel(BlendParams p) {
       if (m > p.list_cap) atomicMax(p.list_overflow, m);
     }
     // ins_argmax stays -1 unless labels were accumulated (raster.cpp:292,497)
-    if (p.n_q == 0 || blend_n == 0 || NCH == 0) p.ins_argmax[pix] = -1;
+    if (p.n_q == 0 || blend_n == 0 || NV == 0) p.ins_argmax[pix] = -1;
   }
 
   // blended_total (raster.cpp:459,502,506): one atomic per warp
@@ -174,72 +294,106 @@ __global__ void __launch_bounds__(kThreads, 2) blend_kernel(BlendParams p) {
     unsigned long long bl = inside ? static_cast<unsigned long long>(blend_n) : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) bl += __shfl_xor_sync(0xffffffffu, bl, o);
-    if ((tid & 31) == 0 && bl) atomicAdd(p.blended_total, bl);
+    if (lane == 0 && bl) atomicAdd(p.blended_total, bl);
   }
 
-  // ---- feature / label planes (raster.cpp:456-499), warp-cooperative
-  if constexpr (NCH > 0) {
+  // ---- feature / label planes (raster.cpp:456-499), warp-cooperative.
+  // LPP lanes serve one pixel (VEC*NV channels each), 32/LPP pixels per iteration:
+  // channel(e, v) = (v * LPP + sub) * VEC + e, so a pixel's run is one coalesced
+  // LPP*VEC*4-byte load per selected surfel and one such store.
+  if constexpr (NV > 0) {
+    constexpr int PPI = 32 / LPP;
     const int D = p.feat_dims;
-    const int lane = tid & 31;
-    const int warp_base = tid & ~31;
-    for (int q = 0; q < 32; ++q) {
-      const int qtid = warp_base + q;
-      const int qx = tx * kTile + (qtid & (kTile - 1));
-      const int qy = ty * kTile + (qtid >> 4);
-      if (qx >= p.width || qy >= p.height) continue;  // warp-uniform
+    const int grp = lane / LPP, sub = lane % LPP;
+    float swf[KMAX > 0 ? KMAX : 1];
+#pragma unroll
+    for (int i = 0; i < (KMAX > 0 ? KMAX : 1); ++i) swf[i] = static_cast<float>(sw[i]);
+    const bool only_sem = p.n_q == 0;
+    for (int q0 = 0; q0 < 32; q0 += PPI) {
+      const int q = q0 + grp;
+      const int qx = wx0 + (q & 7), qy = wy0 + (q >> 3);
+      const bool qin = qx < p.width && qy < p.height;
+      if (!__any_sync(0xffffffffu, qin)) continue;
       const int64_t qpix = static_cast<int64_t>(qy) * p.width + qx;
       int nq = __shfl_sync(0xffffffffu, blend_n, q);
       if constexpr (FULL_LIST) nq = nq < p.list_cap ? nq : p.list_cap;
-      float acc[NCH];
+      if (!qin) nq = 0;
+      float acc[NV][VEC];
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.f;
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[v][e] = 0.f;
+      using TV = typename FVec<VEC>::T;
       if constexpr (KMAX > 0) {
 #pragma unroll
         for (int i = 0; i < KMAX; ++i) {
           const int s = __shfl_sync(0xffffffffu, ss[i], q);
-          const float w = __shfl_sync(0xffffffffu, static_cast<float>(sw[i]), q);
+          const float w = __shfl_sync(0xffffffffu, swf[i], q);
           if (i < nq) {
-            const float* f = p.feat + static_cast<int64_t>(s) * D + lane;
+            const TV* row = reinterpret_cast<const TV*>(p.feat + static_cast<int64_t>(s) * D);
 #pragma unroll
-            for (int ch = 0; ch < NCH; ++ch)
-              if (lane + 32 * ch < D) acc[ch] += w * __ldg(f + 32 * ch);
+            for (int v = 0; v < NV; ++v) {
+              const int idx = v * LPP + sub;
+              if (EXACT || idx * VEC < D) fma_vec<VEC>(acc[v], w, __ldg(row + idx));
+            }
           }
         }
       } else {
         const uint2* lst = p.lists + qpix * p.list_cap;
-        for (int i = 0; i < nq; ++i) {
-          const uint2 e = lst[i];
-          const float w = __uint_as_float(e.y);
-          const float* f = p.feat + static_cast<int64_t>(e.x) * D + lane;
+        for (int i = 0; i < __reduce_max_sync(0xffffffffu, static_cast<unsigned>(nq)); ++i) {
+          if (i < nq) {
+            const uint2 e = lst[i];
+            const TV* row = reinterpret_cast<const TV*>(p.feat + static_cast<int64_t>(e.x) * D);
+            const float w = __uint_as_float(e.y);
 #pragma unroll
-          for (int ch = 0; ch < NCH; ++ch)
-            if (lane + 32 * ch < D) acc[ch] += w * __ldg(f + 32 * ch);
-        }
-      }
-      // lanes own channels lane + 32*ch of the pixel's HWC run: coalesced stores
-      float best = 0.f;
-      int best_i = 0x7fffffff;
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int c = lane + 32 * ch;
-        if (c < D) {
-          const float v = nq > 0 ? acc[ch] : 0.f;
-          if (c < p.c_sem) {
-            if (p.sem_feat) p.sem_feat[qpix * p.c_sem + c] = v;
-          } else {
-            const int qi = c - p.c_sem;
-            if (p.ins_dist) p.ins_dist[qpix * p.n_q + qi] = v;
-            if (best_i == 0x7fffffff || v > best) {  // first max within the lane (ascending index)
-              best = v;
-              best_i = qi;
+            for (int v = 0; v < NV; ++v) {
+              const int idx = v * LPP + sub;
+              if (EXACT || idx * VEC < D) fma_vec<VEC>(acc[v], w, __ldg(row + idx));
             }
           }
         }
       }
-      if (p.n_q > 0 && nq > 0) {
-        // first-max argmax across lanes (raster.cpp:492-497): ties go to the lower index
+      if (only_sem) {
+        if (qin && p.sem_feat) {
+          TV* out = reinterpret_cast<TV*>(p.sem_feat + qpix * D);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+          for (int v = 0; v < NV; ++v) {
+            const int idx = v * LPP + sub;
+            if (EXACT || idx * VEC < D) {
+              TV val;
+              float* f = reinterpret_cast<float*>(&val);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) f[e] = acc[v][e];  // zero when nothing blended
+              out[idx] = val;
+            }
+          }
+        }
+      } else {
+        float best = 0.f;
+        int best_i = 0x7fffffff;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const int c = (v * LPP + sub) * VEC + e;
+            if (qin && c < D) {
+              const float val = acc[v][e];
+              if (c < p.c_sem) {
+                if (p.sem_feat) p.sem_feat[qpix * p.c_sem + c] = val;
+              } else {
+                const int qi = c - p.c_sem;
+                if (p.ins_dist) p.ins_dist[qpix * p.n_q + qi] = val;
+                if (best_i == 0x7fffffff || val > best || (val == best && qi < best_i)) {
+                  best = val;
+                  best_i = qi;
+                }
+              }
+            }
+          }
+        }
+        // first-max argmax across the pixel's LPP lanes (raster.cpp:492-497): ties -> lower index
+#pragma unroll
+        for (int o = LPP / 2; o > 0; o >>= 1) {
           const float ob = __shfl_xor_sync(0xffffffffu, best, o);
           const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
           if (oi != 0x7fffffff && (best_i == 0x7fffffff || ob > best || (ob == best && oi < best_i))) {
@@ -247,28 +401,44 @@ __global__ void __launch_bounds__(kThreads, 2) blend_kernel(BlendParams p) {
             best_i = oi;
           }
         }
-        if (lane == 0) p.ins_argmax[qpix] = best_i;
+        if (sub == 0 && qin && nq > 0) p.ins_argmax[qpix] = best_i;
       }
     }
   }
 }
 
-template <int KMAX, bool FULL, int NCH>
+template <int KMAX, bool FULL, int VEC, int NV, int LPP, bool EXACT>
 void launch_t(const BlendParams& p, int tiles, cudaStream_t st) {
-  blend_kernel<KMAX, FULL, NCH><<<tiles, kThreads, 0, st>>>(p);
+  auto kern = blend_kernel<KMAX, FULL, VEC, NV, LPP, EXACT>;
+  static unsigned long long configured = 0;  // per instantiation, one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured >> dev & 1ull)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    configured |= 1ull << dev;
+  }
+  kern<<<tiles, kThreads, kSmemBytes, st>>>(p);
 }
 
+// Feature-lane shapes: float4 lanes, 32/LPP pixels per warp iteration for the
+// common widths; scalar lanes with guards otherwise.
 template <int KMAX, bool FULL>
-void launch_nch(const BlendParams& p, int nch, int tiles, cudaStream_t st) {
-  switch (nch) {
-    case 0: launch_t<KMAX, FULL, 0>(p, tiles, st); break;
-    case 1: launch_t<KMAX, FULL, 1>(p, tiles, st); break;
-    case 2: launch_t<KMAX, FULL, 2>(p, tiles, st); break;
-    case 3: launch_t<KMAX, FULL, 3>(p, tiles, st); break;
-    case 4: launch_t<KMAX, FULL, 4>(p, tiles, st); break;
-    case 8: launch_t<KMAX, FULL, 8>(p, tiles, st); break;
-    default: launch_t<KMAX, FULL, 16>(p, tiles, st); break;
+void launch_feat(const BlendParams& p, int tiles, cudaStream_t st) {
+  const int D = p.feat_dims;
+  switch (D) {
+    case 0: launch_t<KMAX, FULL, 1, 0, 32, true>(p, tiles, st); return;
+    case 32: launch_t<KMAX, FULL, 4, 1, 8, true>(p, tiles, st); return;
+    case 64: launch_t<KMAX, FULL, 4, 1, 16, true>(p, tiles, st); return;
+    case 96: launch_t<KMAX, FULL, 1, 3, 32, true>(p, tiles, st); return;
+    case 128: launch_t<KMAX, FULL, 4, 1, 32, true>(p, tiles, st); return;
+    case 256: launch_t<KMAX, FULL, 4, 2, 32, true>(p, tiles, st); return;
+    default: break;
   }
+  const int nch = (D + 31) / 32;
+  if (nch <= 2) launch_t<KMAX, FULL, 1, 2, 32, false>(p, tiles, st);
+  else if (nch <= 4) launch_t<KMAX, FULL, 1, 4, 32, false>(p, tiles, st);
+  else if (nch <= 8) launch_t<KMAX, FULL, 1, 8, 32, false>(p, tiles, st);
+  else launch_t<KMAX, FULL, 1, 16, 32, false>(p, tiles, st);
 }
 
 }  // namespace
@@ -282,24 +452,20 @@ int blend_kmax_for(int k_sel) {
 
 int blend_nch_for(int feat_dims) {
   const int c = (feat_dims + 31) / 32;
-  if (c <= 4) return c;
-  if (c <= 8) return 8;
-  if (c <= kMaxNch) return 16;
-  return -1;
+  return c <= 16 ? c : -1;
 }
 
 void launch_blend(const BlendParams& p, int tiles, bool topk, cudaStream_t st) {
   if (tiles <= 0) return;
-  const int nch = blend_nch_for(p.feat_dims);
   if (!topk) {
-    if (nch == 0) launch_t<0, false, 0>(p, tiles, st);
-    else launch_nch<0, true>(p, nch, tiles, st);
+    if (p.feat_dims == 0) launch_t<0, false, 1, 0, 32, true>(p, tiles, st);
+    else launch_feat<0, true>(p, tiles, st);
     return;
   }
   switch (blend_kmax_for(p.k_sel)) {
-    case 8: launch_nch<8, false>(p, nch, tiles, st); break;
-    case 16: launch_nch<16, false>(p, nch, tiles, st); break;
-    default: launch_nch<32, false>(p, nch, tiles, st); break;
+    case 8: launch_feat<8, false>(p, tiles, st); break;
+    case 16: launch_feat<16, false>(p, tiles, st); break;
+    default: launch_feat<32, false>(p, tiles, st); break;
   }
 }
 

@@ -49,43 +49,67 @@ PSM_HD double psm_fma(double a, double b, double c) {
 #endif
 }
 
+// exp(r) coefficients 1/n!, n = 13 .. 0 (Horner order). On the device they live in
+// the constant bank so each DFMA takes its coefficient as a c[] operand instead of
+// re-materialising a 64-bit immediate; the values (hence the bits) are identical.
+#define PSM_EXP_COEFFS                                                                     \
+  {1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,                    \
+   2.755731922398589e-07, 2.7557319223985893e-06, 2.48015873015873e-05,                    \
+   0.0001984126984126984, 0.001388888888888889, 0.008333333333333333,                      \
+   0.041666666666666664, 0.16666666666666666, 0.5, 1.0, 1.0}
+#if defined(__CUDACC__)
+static __constant__ double psm_exp_c_dev[14] = PSM_EXP_COEFFS;
+#endif
+static const double psm_exp_c_host[14] = PSM_EXP_COEFFS;
+
+// exp(r) for the reduced argument r, times 2^k, k = rint(x / ln2). Shared tail of
+// psm_exp and psm_exp_nonpos.
+PSM_HD double psm_exp_core(double x, double t) {
+  const double kShift = 6755399441055744.0;       // 1.5 * 2^52: add/sub rounds to integer (ties-even)
+  const double kLn2Hi = 0.6931471803691238;       // 0x3fe62e42fee00000, k*kLn2Hi exact for |k| < 2^11
+  const double kLn2Lo = 1.9082149292705877e-10;
+  const double ks = t + kShift;
+  const double kd = ks - kShift;
+  // k from the low mantissa bits of ks (two's complement of k): no float->int conversion
+#if defined(__CUDA_ARCH__)
+  const int k = __double2loint(ks);
+  const double* c = psm_exp_c_dev;
+#else
+  uint64_t ksb;
+  memcpy(&ksb, &ks, sizeof ksb);
+  const int k = (int)(uint32_t)(ksb & 0xffffffffu);
+  const double* c = psm_exp_c_host;
+#endif
+  double r = psm_fma(-kd, kLn2Hi, x);
+  r = psm_fma(-kd, kLn2Lo, r);
+  double p = c[0];
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+  for (int i = 1; i < 14; ++i) p = psm_fma(p, r, c[i]);
+  if (k > 1023) {  // only reachable for x within ~0.35 of the overflow bound
+    return (p * 2.0) * psm_bits_to_double((uint64_t)(k - 1 + 1023) << 52);
+  }
+  if (k >= -1021) {
+    return p * psm_bits_to_double((uint64_t)(k + 1023) << 52);
+  }
+  // subnormal result: scale in two exact-then-rounded steps
+  return (p * psm_bits_to_double((uint64_t)(k + 1023 + 64) << 52)) *
+         psm_bits_to_double((uint64_t)(1023 - 64) << 52);
+}
+
 PSM_HD double psm_exp(double x) {
   if (x != x) return x + x;                       // NaN propagates
   if (x > 709.782712893384) return 1.0 / 0.0;     // overflow -> +inf
   if (x < -745.1332191019412) return 0.0;         // below half the smallest subnormal
-  const double kLog2e = 1.4426950408889634;
-  const double kShift = 6755399441055744.0;       // 1.5 * 2^52: add/sub rounds to integer (ties-even)
-  const double kLn2Hi = 0.6931471803691238;       // 0x3fe62e42fee00000, k*kLn2Hi exact for |k| < 2^11
-  const double kLn2Lo = 1.9082149292705877e-10;
-  double t = x * kLog2e;
-  double kd = t + kShift;
-  kd = kd - kShift;
-  const int k = static_cast<int>(kd);
-  double r = psm_fma(-kd, kLn2Hi, x);
-  r = psm_fma(-kd, kLn2Lo, r);
-  double p = 1.6059043836821613e-10;              // 1/13!
-  p = psm_fma(p, r, 2.08767569878681e-09);        // 1/12!
-  p = psm_fma(p, r, 2.505210838544172e-08);       // 1/11!
-  p = psm_fma(p, r, 2.755731922398589e-07);       // 1/10!
-  p = psm_fma(p, r, 2.7557319223985893e-06);      // 1/9!
-  p = psm_fma(p, r, 2.48015873015873e-05);        // 1/8!
-  p = psm_fma(p, r, 0.0001984126984126984);       // 1/7!
-  p = psm_fma(p, r, 0.001388888888888889);        // 1/6!
-  p = psm_fma(p, r, 0.008333333333333333);        // 1/5!
-  p = psm_fma(p, r, 0.041666666666666664);        // 1/4!
-  p = psm_fma(p, r, 0.16666666666666666);         // 1/3!
-  p = psm_fma(p, r, 0.5);                         // 1/2!
-  p = psm_fma(p, r, 1.0);                         // 1/1!
-  p = psm_fma(p, r, 1.0);                         // 1/0!
-  if (k > 1023) {  // only reachable for x within ~0.35 of the overflow bound
-    return (p * 2.0) * psm_bits_to_double(static_cast<uint64_t>(k - 1 + 1023) << 52);
-  }
-  if (k >= -1021) {
-    return p * psm_bits_to_double(static_cast<uint64_t>(k + 1023) << 52);
-  }
-  // subnormal result: scale in two exact-then-rounded steps
-  return (p * psm_bits_to_double(static_cast<uint64_t>(k + 1023 + 64) << 52)) *
-         psm_bits_to_double(static_cast<uint64_t>(1023 - 64) << 52);
+  return psm_exp_core(x, x * 1.4426950408889634);
+}
+
+// psm_exp restricted to x <= 0 or NaN (the alpha argument -0.5 (u^2 + v^2)):
+// same bits as psm_exp there, without the overflow branch.
+PSM_HD double psm_exp_nonpos(double x) {
+  if (!(x >= -745.1332191019412)) return x != x ? x + x : 0.0;
+  return psm_exp_core(x, x * 1.4426950408889634);
 }
 
 #endif  // PSM_EXP_H
