@@ -46,9 +46,10 @@ struct __align__(16) WarpStage {
 };
 constexpr size_t kSmemBytes = sizeof(WarpStage) * kWarps;
 
-// before(a, b) of topk_select (raster.cpp:232-235), proj order == source order
-__device__ __forceinline__ bool before(double wa, int sa, double wb, int sb) {
-  return wa > wb || (wa == wb && sa < sb);
+// before(a, b) of topk_select (raster.cpp:232-235), proj order == source order.
+// Slots hold list positions; the source ids are only looked up on an exact weight tie.
+__device__ __forceinline__ bool before(double wa, int pa, double wb, int pb, const uint32_t* __restrict__ vals) {
+  return wa > wb || (wa == wb && __ldg(vals + pa) < __ldg(vals + pb));
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -94,38 +95,22 @@ __device__ __forceinline__ void accumulate_row(float (&acc)[NV][VEC], float w, c
   }
 }
 
-// Can the support ellipse d^T Finv d <= chi2 of record r reach any pixel centre of
-// the warp's block [x0, x1] x [y0, y1]? Continuous minimum of the quadratic over
-// the rectangle (on its boundary when the centre lies outside), compared with a
-// relative 1e-6 margin so the per-pixel fp64 test (raster.cpp:379) can never pass
-// where this says no; ill-conditioned or non-finite footprints always pass.
-__device__ __forceinline__ bool block_meets(const SurfRec& r, double x0, double x1, double y0, double y1,
-                                            double chi2lim) {
-  const double ax = x0 - r.cx, bx = x1 - r.cx, ay = y0 - r.cy, by = y1 - r.cy;
-  if (!(ax > 0.0 || bx < 0.0 || ay > 0.0 || by < 0.0)) return true;  // centre inside (or NaN)
-  const double a = r.f00, b2 = r.f01x2, c = r.f11;
-  const double det = a * c - 0.25 * b2 * b2;
-  if (!(det > 0.0) || !((a + c) * (a + c) < 1e12 * det)) return true;
-  double best = 1e300;
-  {
-    const double ia = -0.5 * b2 / c;  // argmin dy on a vertical edge is ia * X
-    double dy = ia * ax;
-    dy = fmin(fmax(dy, ay), by);
-    best = fmin(best, (a * ax + b2 * dy) * ax + c * dy * dy);
-    dy = ia * bx;
-    dy = fmin(fmax(dy, ay), by);
-    best = fmin(best, (a * bx + b2 * dy) * bx + c * dy * dy);
-  }
-  {
-    const double ic = -0.5 * b2 / a;  // argmin dx on a horizontal edge is ic * Y
-    double dx = ic * ay;
-    dx = fmin(fmax(dx, ax), bx);
-    best = fmin(best, (c * ay + b2 * dx) * ay + a * dx * dx);
-    dx = ic * by;
-    dx = fmin(fmax(dx, ax), bx);
-    best = fmin(best, (c * by + b2 * dx) * by + a * dx * dx);
-  }
-  return !(best > chi2lim);
+// Can the (inflated) support ellipse of a candidate reach any pixel centre of the
+// warp's block [x0, x1] x [y0, y1] (already widened by the absolute margin)? The
+// ellipse's x-extent over the strip dy in [y0 - cy, y1 - cy] is its right edge
+// slope*dy + sqrt((kF11 - dy^2) dq) at the concave maximiser dstar clamped into the
+// strip (left edge: -dstar), as in psm_ellipse.h. fp32 with k inflated by 1e-4 and a
+// 0.02 px margin: conservative against the per-pixel fp64 test (raster.cpp:379).
+__device__ __forceinline__ bool cull_meets(const float4 a, const float4 b, float x0, float x1, float y0, float y1) {
+  const float cx = a.x, cy = a.y, ey = a.z, slope = a.w, dstar = b.x, kf11 = b.y, dq = b.z;
+  if (!(ey < __int_as_float(0x7f800000))) return true;  // ill-conditioned / non-finite: keep
+  const float dlo = fmaxf(y0 - cy, -ey), dhi = fminf(y1 - cy, ey);
+  if (dlo > dhi) return false;
+  const float dr = fminf(fmaxf(dstar, dlo), dhi);
+  const float dl = fminf(fmaxf(-dstar, dlo), dhi);
+  const float xr = cx + slope * dr + sqrtf(fmaxf(kf11 - dr * dr, 0.f) * dq);
+  const float xl = cx + slope * dl - sqrtf(fmaxf(kf11 - dl * dl, 0.f) * dq);
+  return xl <= x1 && xr >= x0;
 }
 
 // Resident CTAs per SM: 3 (80 registers) for K <= 8, fewer for the wider register Top-K.
@@ -148,10 +133,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   const int64_t pix = static_cast<int64_t>(y) * p.width + x;
 
   const double px = x + 0.5, py = y + 0.5;
-  // pixel-centre extents of the warp's 8x4 block (clipped to the image) for the prefilter
-  const double bx0 = wx0 + 0.5, by0 = wy0 + 0.5;
-  const double bx1 = min(wx0 + 8, p.width) - 0.5, by1 = min(wy0 + 4, p.height) - 0.5;
-  const double chi2lim = p.chi2 * 1.000001 + 1e-9;
+  // pixel-centre extents of the warp's 8x4 block (clipped to the image), widened by
+  // the prefilter's 0.02 px margin
+  const float bx0 = wx0 + 0.48f, by0 = wy0 + 0.48f;
+  const float bx1 = min(wx0 + 8, p.width) - 0.48f, by1 = min(wy0 + 4, p.height) - 0.48f;
   const double rx = (px - p.cam_cx) / p.cam_fx;  // division as in raster.cpp:370-371
   const double ry = (py - p.cam_cy) / p.cam_fy;
 
@@ -165,13 +150,17 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
 #pragma unroll
   for (int i = 0; i < (KMAX > 0 ? KMAX : 1); ++i) {
     sw[i] = -1.0;
-    ss[i] = 0x7fffffff;
+    ss[i] = 0;  // list position; never compared (weights are > 0)
   }
 
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
+  float4 cn0 = make_float4(0.f, 0.f, 0.f, 0.f), cn1 = cn0;  // next chunk's prefilter record (lane's candidate)
   auto prefetch = [&](int base, int buf) {
     if (base + lane < end) {
       const int s = static_cast<int>(__ldg(p.vals + base + lane));
+      const float4* cr = reinterpret_cast<const float4*>(p.culls + s);
+      cn0 = __ldg(cr);
+      cn1 = __ldg(cr + 1);
       const char* g = reinterpret_cast<const char*>(p.recs + s);
       char* d = reinterpret_cast<char*>(&stage.rec[buf][lane]);
 #pragma unroll
@@ -185,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   for (int base = start; base < end; base += kChunk, buf ^= 1) {
     if (__all_sync(0xffffffffu, done)) break;
     const int cnt = min(kChunk, end - base);
+    const float4 c0 = cn0, c1 = cn1;
     if (base + kChunk < end) {
       prefetch(base + kChunk, buf ^ 1);
       cp_async_wait<1>();
@@ -195,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
     const SurfRec* recs = stage.rec[buf];
     // candidates that reach no pixel centre of this warp's block are skipped as a whole
     unsigned live = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
-    if (p.support_cutoff) live = __ballot_sync(0xffffffffu, lane < cnt && block_meets(recs[lane], bx0, bx1, by0, by1, chi2lim));
+    if (p.support_cutoff) live = __ballot_sync(0xffffffffu, lane < cnt && cull_meets(c0, c1, bx0, bx1, by0, by1));
     if (!done) {
       while (live) {
         const int j = __ffs(live) - 1;
@@ -228,25 +218,25 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
           dom_w = wt;
           dom_depth = rcp;
         }
-        const int src = static_cast<int>(__ldg(p.vals + base + j));
+        const int pos = base + j;  // list position; source id = vals[pos]
         if constexpr (KMAX > 0) {
-          if (before(wt, src, sw[KMAX - 1], ss[KMAX - 1])) {
+          if (before(wt, pos, sw[KMAX - 1], ss[KMAX - 1], p.vals)) {
 #pragma unroll
             for (int i = KMAX - 1; i > 0; --i) {
-              if (before(wt, src, sw[i], ss[i])) {
-                const bool above_prev = before(wt, src, sw[i - 1], ss[i - 1]);
+              if (before(wt, pos, sw[i], ss[i], p.vals)) {
+                const bool above_prev = before(wt, pos, sw[i - 1], ss[i - 1], p.vals);
                 sw[i] = above_prev ? sw[i - 1] : wt;
-                ss[i] = above_prev ? ss[i - 1] : src;
+                ss[i] = above_prev ? ss[i - 1] : pos;
               }
             }
-            if (before(wt, src, sw[0], ss[0])) {
+            if (before(wt, pos, sw[0], ss[0], p.vals)) {
               sw[0] = wt;
-              ss[0] = src;
+              ss[0] = pos;
             }
           }
         }
         if constexpr (FULL_LIST) {
-          if (m < p.list_cap) p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(src), __float_as_uint(wf));
+          if (m < p.list_cap) p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(pos), __float_as_uint(wf));
         }
         T *= 1.0 - alpha;
         ++m;
@@ -260,6 +250,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   }
   cp_async_wait<0>();
 
+  if constexpr (KMAX > 0) {
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) ss[i] = sw[i] > 0.0 ? static_cast<int>(__ldg(p.vals + ss[i])) : -1;
+  }
   const int k_sel = p.k_sel;
   int blend_n = m;
   if constexpr (KMAX > 0) blend_n = m < k_sel ? m : k_sel;
@@ -343,7 +337,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
         for (int i = 0; i < __reduce_max_sync(0xffffffffu, static_cast<unsigned>(nq)); ++i) {
           if (i < nq) {
             const uint2 e = lst[i];
-            const TV* row = reinterpret_cast<const TV*>(p.feat + static_cast<int64_t>(e.x) * D);
+            const uint32_t src = __ldg(p.vals + e.x);
+            const TV* row = reinterpret_cast<const TV*>(p.feat + static_cast<int64_t>(src) * D);
             const float w = __uint_as_float(e.y);
 #pragma unroll
             for (int v = 0; v < NV; ++v) {

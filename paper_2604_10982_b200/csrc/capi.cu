@@ -51,7 +51,7 @@ struct psm_ctx {
   psm_stage_times times{};
   psm_counters last{};
   // scratch
-  psm::Buf recs, bins, depth_bits, tile_cnt, valid, pos, keys_c, src_c, keys_s, src_s, cnt_rank, off_rank;
+  psm::Buf recs, bins, culls, depth_bits, tile_cnt, valid, pos, keys_c, src_c, keys_s, src_s, cnt_rank, off_rank;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, cub_tmp, dev_small, lists, rank_of, dbg_keys, topk_dbg;
   psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
   int64_t* h_small = nullptr;  // pinned: counters read-back
@@ -180,14 +180,15 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   uint32_t* tvals_s = nullptr;
   uint32_t* tkeys_s = nullptr;
   if (n > 0) {
-    SurfRec* recs; BinRec* bins; uint64_t* dbits; int32_t *tcnt, *valid, *pos;
+    SurfRec* recs; BinRec* bins; CullRec* culls; uint64_t* dbits; int32_t *tcnt, *valid, *pos;
     PSM_TRY(ensure(ctx, ctx->recs, n, &recs));
     PSM_TRY(ensure(ctx, ctx->bins, n, &bins));
+    PSM_TRY(ensure(ctx, ctx->culls, n, &culls));
     PSM_TRY(ensure(ctx, ctx->depth_bits, n, &dbits));
     PSM_TRY(ensure(ctx, ctx->tile_cnt, n, &tcnt));
     PSM_TRY(ensure(ctx, ctx->valid, n, &valid));
     PSM_TRY(ensure(ctx, ctx->pos, n, &pos));
-    launch_preprocess(sc->surfels, n, dc, rs, recs, bins, dbits, tcnt, valid, reinterpret_cast<int32_t*>(small), st);
+    launch_preprocess(sc->surfels, n, dc, rs, recs, bins, culls, dbits, tcnt, valid, reinterpret_cast<int32_t*>(small), st);
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 1);
 
@@ -270,6 +271,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   bp.ranges = ranges;
   bp.vals = tvals_s;
   bp.recs = static_cast<const SurfRec*>(ctx->recs.p);
+  bp.culls = static_cast<const CullRec*>(ctx->culls.p);
   bp.feat = sc->feat;
   bp.feat_dims = feat_dims; bp.c_sem = sc->c_sem; bp.n_q = sc->n_q;
   bp.width = W; bp.height = H; bp.tiles_x = tiles_x;
@@ -464,7 +466,7 @@ int psm_destroy(psm_ctx* ctx) {
   if (!ctx) return PSM_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->depth_bits, &ctx->tile_cnt, &ctx->valid, &ctx->pos,
+  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->culls, &ctx->depth_bits, &ctx->tile_cnt, &ctx->valid, &ctx->pos,
                       &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s, &ctx->cnt_rank, &ctx->off_rank,
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->cub_tmp,
                       &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,

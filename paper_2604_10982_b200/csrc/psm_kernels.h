@@ -13,6 +13,7 @@ struct BlendParams {
   const int32_t* ranges;  // [tiles][2]
   const uint32_t* vals;   // tile-sorted source ids
   const SurfRec* recs;
+  const CullRec* culls;
   const float* feat;      // [N][feat_dims]: f_sem | labels, fp32
   int32_t feat_dims, c_sem, n_q;
   int32_t width, height, tiles_x;
@@ -30,8 +31,8 @@ struct BlendParams {
 
 // K1 preprocess.cu
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
-                       BinRec* bins, uint64_t* depth_bits, int32_t* tile_cnt, int32_t* valid, int32_t* err,
-                       cudaStream_t stream);
+                       BinRec* bins, CullRec* culls, uint64_t* depth_bits, int32_t* tile_cnt, int32_t* valid,
+                       int32_t* err, cudaStream_t stream);
 
 // binning.cu
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n,
