@@ -464,6 +464,11 @@ void oracle_psm_exp(const double* x, int64_t n, double* out) {
   for (int64_t i = 0; i < n; ++i) out[i] = psm_exp(x[i]);
 }
 
+// glibc exp exactly as the reference calls it (raster.cpp:390), for the libm pin.
+void oracle_libm_exp(const double* x, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = std::exp(x[i]);
+}
+
 // topk_select over explicit keys (raster.cpp:225-251); selected[m] out.
 void oracle_topk_select(const double* weights, const int32_t* proj, int32_t m, int32_t k, int8_t* selected) {
   std::vector<WeightKey> keys(m), best;

@@ -131,6 +131,26 @@ def psm_exp(x) -> np.ndarray:
     return out
 
 
+def libm_exp(x) -> np.ndarray:
+    """glibc exp (the reference's libm), called from C++ std::exp."""
+    xs = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    out = np.empty_like(xs)
+    fn = load().oracle_libm_exp
+    fn.restype = None
+    fn.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
+    fn(_p(xs), xs.size, _p(out))
+    return out
+
+
+def host_uses_fma_exp() -> bool:
+    """glibc's ifunc picks the FMA build of exp on CPUs with FMA and AVX2."""
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+    return " fma" in flags and " avx2" in flags
+
+
 def topk_select(weights, proj, k: int) -> np.ndarray:
     w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
     p = np.ascontiguousarray(np.asarray(proj, dtype=np.int32))

@@ -1,27 +1,35 @@
 // psm_exp.h — the one libm function on the render hot path, restated so that
-// the CUDA kernels and the CPU oracle produce the same bits.
+// the CUDA kernels, the CPU oracle and the reference's own glibc produce the
+// same bits.
 //
 // The reference evaluates alpha = o * std::exp(-0.5 * (u*u + v*v)) with glibc
-// `exp` (proj/src/raster.cpp:390, :175). glibc picks an FMA or non-FMA variant
-// at load time (ifunc), so its last bit already depends on the host CPU, and
-// CUDA's device `exp` is a third implementation. Every decision the renderer
-// makes (alpha >= alpha_min, T < t_min, Top-K order by weight) is taken on
-// this value, so bit-exact parity needs one exp evaluated identically on both
-// sides. This one uses only IEEE-754 double add/mul and explicit fused
-// multiply-adds (fma is correctly rounded on x86-64 and on sm_100a), in a fixed
-// order, so host and device results are identical by construction.
+// `exp` (proj/src/raster.cpp:390, :175). Every decision the renderer makes
+// (alpha >= alpha_min, T < t_min, Top-K order by weight) is taken on that value,
+// so bit-exact parity needs one exp evaluated identically everywhere.
 //
-// Algorithm: exp(x) = 2^k * exp(r), k = rint(x / ln2), r = x - k*ln2 with a
-// two-term (Cody–Waite) ln2; exp(r) by the degree-13 Taylor polynomial in
-// Horner/FMA form (|r| <= 0.347, truncation < 5e-18 relative). Measured error
-// against glibc: tests/test_oracle_kat.py::test_psm_exp_vs_glibc (<= 1 ulp).
+// glibc >= 2.28 implements exp with the optimized-routines algorithm
+// (sysdeps/ieee754/dbl-64/e_exp.c + e_exp_data.c; third-party dependency of the
+// reference, not vendored in /root/reference): exp(x) = 2^(k/128) * exp(r),
+// k = rint(x * 128/ln2), r = x - k ln2/128 (two-term ln2), 2^(k/128) from a
+// 128-entry table {tail, scale bits}, exp(r) - 1 by a degree-5 polynomial,
+// result scale + scale * tmp. On x86-64 hosts with FMA+AVX2 (this image and the
+// GPU boxes) the ifunc selects the -mfma build (__exp_fma); the operation
+// order below is that build's, read off the image's libm.so.6 disassembly
+// (fused: kd, both r steps, the three polynomial combinations, the final
+// scale + scale*tmp; k < 0 special case unfused as compiled). The constants are
+// the published e_exp_data.c values; the table is regenerated from its
+// definition by gen_exp_table.py. tests/test_oracle_kat.py::test_psm_exp_is_glibc_exp
+// checks bit equality with the host glibc exp on millions of arguments.
 //
-// Compile with contraction disabled (host: -ffp-contract=off; device:
-// --fmad=false) so the non-fused products below are not fused behind our back.
+// Only IEEE-754 add/mul and explicit fused multiply-adds are used (fma is
+// correctly rounded on x86-64 and on sm_100a). Compile with contraction off
+// (host: -ffp-contract=off; device: --fmad=false) so nothing else is fused.
 #ifndef PSM_EXP_H
 #define PSM_EXP_H
 
 #include <stdint.h>
+
+#include "psm_exp_table.h"
 
 #if defined(__CUDACC__)
 #define PSM_HD __host__ __device__ __forceinline__
@@ -41,6 +49,16 @@ PSM_HD double psm_bits_to_double(uint64_t b) {
 #endif
 }
 
+PSM_HD uint64_t psm_double_to_bits(double d) {
+#if defined(__CUDA_ARCH__)
+  return static_cast<uint64_t>(__double_as_longlong(d));
+#else
+  uint64_t b;
+  memcpy(&b, &d, sizeof b);
+  return b;
+#endif
+}
+
 PSM_HD double psm_fma(double a, double b, double c) {
 #if defined(__CUDA_ARCH__)
   return __fma_rn(a, b, c);
@@ -49,67 +67,86 @@ PSM_HD double psm_fma(double a, double b, double c) {
 #endif
 }
 
-// exp(r) coefficients 1/n!, n = 13 .. 0 (Horner order). On the device they live in
-// the constant bank so each DFMA takes its coefficient as a c[] operand instead of
-// re-materialising a 64-bit immediate; the values (hence the bits) are identical.
-#define PSM_EXP_COEFFS                                                                     \
-  {1.6059043836821613e-10, 2.08767569878681e-09, 2.505210838544172e-08,                    \
-   2.755731922398589e-07, 2.7557319223985893e-06, 2.48015873015873e-05,                    \
-   0.0001984126984126984, 0.001388888888888889, 0.008333333333333333,                      \
-   0.041666666666666664, 0.16666666666666666, 0.5, 1.0, 1.0}
+// {tail_i, bits(2^(i/128)) - (i << 45)}, i = 0..127 (2 KB; L1-resident on the device)
 #if defined(__CUDACC__)
-static __constant__ double psm_exp_c_dev[14] = PSM_EXP_COEFFS;
+static __device__ const uint64_t psm_exp_tab_dev[256] = PSM_EXP_TABLE_INIT;
 #endif
-static const double psm_exp_c_host[14] = PSM_EXP_COEFFS;
+static const uint64_t psm_exp_tab_host[256] = PSM_EXP_TABLE_INIT;
 
-// exp(r) for the reduced argument r, times 2^k, k = rint(x / ln2). Shared tail of
-// psm_exp and psm_exp_nonpos.
-PSM_HD double psm_exp_core(double x, double t) {
-  const double kShift = 6755399441055744.0;       // 1.5 * 2^52: add/sub rounds to integer (ties-even)
-  const double kLn2Hi = 0.6931471803691238;       // 0x3fe62e42fee00000, k*kLn2Hi exact for |k| < 2^11
-  const double kLn2Lo = 1.9082149292705877e-10;
-  const double ks = t + kShift;
-  const double kd = ks - kShift;
-  // k from the low mantissa bits of ks (two's complement of k): no float->int conversion
+PSM_HD void psm_exp_tab(uint64_t idx, double* tail, uint64_t* sbits_hi) {
 #if defined(__CUDA_ARCH__)
-  const int k = __double2loint(ks);
-  const double* c = psm_exp_c_dev;
+  const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(psm_exp_tab_dev) + (idx >> 1));
+  *tail = psm_bits_to_double(e.x);
+  *sbits_hi = e.y;
 #else
-  uint64_t ksb;
-  memcpy(&ksb, &ks, sizeof ksb);
-  const int k = (int)(uint32_t)(ksb & 0xffffffffu);
-  const double* c = psm_exp_c_host;
+  *tail = psm_bits_to_double(psm_exp_tab_host[idx]);
+  *sbits_hi = psm_exp_tab_host[idx + 1];
 #endif
-  double r = psm_fma(-kd, kLn2Hi, x);
-  r = psm_fma(-kd, kLn2Lo, r);
-  double p = c[0];
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-  for (int i = 1; i < 14; ++i) p = psm_fma(p, r, c[i]);
-  if (k > 1023) {  // only reachable for x within ~0.35 of the overflow bound
-    return (p * 2.0) * psm_bits_to_double((uint64_t)(k - 1 + 1023) << 52);
+}
+
+// e_exp.c specialcase(): |x| in [512, 1024) where the scale leaves the normal range.
+PSM_HD double psm_exp_special(double tmp, uint64_t sbits, uint64_t ki) {
+  if ((ki & 0x80000000u) == 0) {  // k > 0: scale down by 2^1009, result may overflow
+    sbits -= 1009ull << 52;
+    const double scale = psm_bits_to_double(sbits);
+    return 0x1p1009 * psm_fma(scale, tmp, scale);
   }
-  if (k >= -1021) {
-    return p * psm_bits_to_double((uint64_t)(k + 1023) << 52);
+  // k < 0: the result may be subnormal; round it once (unfused, as compiled)
+  sbits += 1022ull << 52;
+  const double scale = psm_bits_to_double(sbits);
+  const double st = scale * tmp;
+  double y = scale + st;
+  if (y < 1.0) {
+    double lo = scale - y + st;
+    const double hi = 1.0 + y;
+    lo = 1.0 - hi + y + lo;
+    y = (lo + hi) - 1.0;
+    if (y == 0.0) y = 0.0;
   }
-  // subnormal result: scale in two exact-then-rounded steps
-  return (p * psm_bits_to_double((uint64_t)(k + 1023 + 64) << 52)) *
-         psm_bits_to_double((uint64_t)(1023 - 64) << 52);
+  return 0x1p-1022 * y;
 }
 
 PSM_HD double psm_exp(double x) {
-  if (x != x) return x + x;                       // NaN propagates
-  if (x > 709.782712893384) return 1.0 / 0.0;     // overflow -> +inf
-  if (x < -745.1332191019412) return 0.0;         // below half the smallest subnormal
-  return psm_exp_core(x, x * 1.4426950408889634);
+  const double kInvLn2N = 0x1.71547652b82fep7;   // 128 / ln2
+  const double kShift = 0x1.8p52;
+  const double kNegLn2HiN = -0x1.62e42fefa0000p-8;
+  const double kNegLn2LoN = -0x1.cf79abc9e3b3ap-47;
+  const double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
+  const double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+  const uint64_t ix = psm_double_to_bits(x);
+  uint32_t abstop = static_cast<uint32_t>(ix >> 52) & 0x7ffu;
+  if (abstop - 0x3c9u >= 0x3fu) {                      // |x| < 2^-54, |x| >= 512, inf or nan
+    if (static_cast<int32_t>(abstop - 0x3c9u) < 0) return 1.0 + x;  // tiny: rounds to 1
+    if (abstop >= 0x409u) {                            // |x| >= 1024
+      if (ix == 0xfff0000000000000ull) return 0.0;     // -inf
+      if (abstop >= 0x7ffu) return 1.0 + x;            // +inf or nan
+      return (ix >> 63) ? 0.0 : psm_bits_to_double(0x7ff0000000000000ull);  // underflow to +0 / overflow to +inf
+    }
+    abstop = 0;                                        // 512 <= |x| < 1024: special-cased below
+  }
+  double kd = psm_fma(x, kInvLn2N, kShift);
+  const uint64_t ki = psm_double_to_bits(kd);
+  kd = kd - kShift;
+  double r = psm_fma(kd, kNegLn2HiN, x);
+  r = psm_fma(kd, kNegLn2LoN, r);
+  const uint64_t idx = 2 * (ki % 128);
+  const uint64_t top = ki << 45;
+  double tail;
+  uint64_t sbits;
+  psm_exp_tab(idx, &tail, &sbits);
+  sbits += top;
+  const double r2 = r * r;
+  const double a = psm_fma(r, C3, C2);
+  const double t1 = psm_fma(a, r2, r + tail);
+  const double b = psm_fma(r, C5, C4);
+  const double r4 = r2 * r2;
+  const double tmp = psm_fma(r4, b, t1);
+  if (abstop == 0) return psm_exp_special(tmp, sbits, ki);
+  const double scale = psm_bits_to_double(sbits);
+  return psm_fma(scale, tmp, scale);
 }
 
-// psm_exp restricted to x <= 0 or NaN (the alpha argument -0.5 (u^2 + v^2)):
-// same bits as psm_exp there, without the overflow branch.
-PSM_HD double psm_exp_nonpos(double x) {
-  if (!(x >= -745.1332191019412)) return x != x ? x + x : 0.0;
-  return psm_exp_core(x, x * 1.4426950408889634);
-}
+// The alpha argument -0.5 (u^2 + v^2) is <= 0 or NaN; psm_exp is the whole story.
+PSM_HD double psm_exp_nonpos(double x) { return psm_exp(x); }
 
 #endif  // PSM_EXP_H
