@@ -38,13 +38,14 @@ namespace {
 constexpr int kTile = 16;
 constexpr int kThreads = kTile * kTile;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 32;                   // records per warp chunk
+constexpr int kChunk = 30;                   // records per warp chunk (30: the exp table fits 3 CTAs/SM)
 constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
 
 struct __align__(16) WarpStage {
   SurfRec rec[2][kChunk];
 };
-constexpr size_t kSmemBytes = sizeof(WarpStage) * kWarps;
+constexpr size_t kExpTabBytes = 256 * sizeof(uint64_t);
+constexpr size_t kSmemBytes = sizeof(WarpStage) * kWarps + kExpTabBytes;
 
 // before(a, b) of topk_select (raster.cpp:232-235), proj order == source order.
 // Slots hold list positions; the source ids are only looked up on an exact weight tie.
@@ -120,6 +121,10 @@ template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT>
 __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(BlendParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpStage& stage = reinterpret_cast<WarpStage*>(smem_raw)[threadIdx.x >> 5];
+  // psm_exp's 2^(i/128) table, one copy per CTA (random per-lane lookups: shared memory, not L1)
+  uint64_t* exp_tab = reinterpret_cast<uint64_t*>(smem_raw + sizeof(WarpStage) * kWarps);
+  exp_tab[threadIdx.x] = psm_exp_tab_dev[threadIdx.x];
+  __syncthreads();
 
   const int tile = blockIdx.x;
   const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
   float4 cn0 = make_float4(0.f, 0.f, 0.f, 0.f), cn1 = cn0;  // next chunk's prefilter record (lane's candidate)
   auto prefetch = [&](int base, int buf) {
-    if (base + lane < end) {
+    if (lane < kChunk && base + lane < end) {
       const int s = static_cast<int>(__ldg(p.vals + base + lane));
       const float4* cr = reinterpret_cast<const float4*>(p.culls + s);
       cn0 = __ldg(cr);
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
     __syncwarp();
     const SurfRec* recs = stage.rec[buf];
     // candidates that reach no pixel centre of this warp's block are skipped as a whole
-    unsigned live = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+    unsigned live = (1u << cnt) - 1u;  // cnt <= 30
     if (p.support_cutoff) live = __ballot_sync(0xffffffffu, lane < cnt && cull_meets(c0, c1, bx0, bx1, by0, by1));
     if (!done) {
       while (live) {
@@ -202,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
         if (!(w2 > 1e-14)) continue;
         const double rcp = 1.0 / w2;
         const double u = w0 * rcp, v = w1 * rcp;
-        const double alpha = r.opacity * psm_exp_nonpos(-0.5 * (u * u + v * v));
+        const double alpha = r.opacity * psm_exp_t(-0.5 * (u * u + v * v), exp_tab);
         if (alpha < p.alpha_min || alpha <= 0.0) continue;
         const double wt = alpha * T;
         // colour / depth / normal always over the full list (raster.cpp:405-436)

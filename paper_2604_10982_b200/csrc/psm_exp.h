@@ -73,14 +73,14 @@ static __device__ const uint64_t psm_exp_tab_dev[256] = PSM_EXP_TABLE_INIT;
 #endif
 static const uint64_t psm_exp_tab_host[256] = PSM_EXP_TABLE_INIT;
 
-PSM_HD void psm_exp_tab(uint64_t idx, double* tail, uint64_t* sbits_hi) {
+PSM_HD void psm_exp_tab(const uint64_t* tab, uint64_t idx, double* tail, uint64_t* sbits_hi) {
 #if defined(__CUDA_ARCH__)
-  const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(psm_exp_tab_dev) + (idx >> 1));
+  const ulonglong2 e = reinterpret_cast<const ulonglong2*>(tab)[idx >> 1];
   *tail = psm_bits_to_double(e.x);
   *sbits_hi = e.y;
 #else
-  *tail = psm_bits_to_double(psm_exp_tab_host[idx]);
-  *sbits_hi = psm_exp_tab_host[idx + 1];
+  *tail = psm_bits_to_double(tab[idx]);
+  *sbits_hi = tab[idx + 1];
 #endif
 }
 
@@ -106,7 +106,8 @@ PSM_HD double psm_exp_special(double tmp, uint64_t sbits, uint64_t ki) {
   return 0x1p-1022 * y;
 }
 
-PSM_HD double psm_exp(double x) {
+// `tab` is the 256-word table (psm_exp_tab_dev, a shared-memory copy of it, or the host array).
+PSM_HD double psm_exp_t(double x, const uint64_t* tab) {
   const double kInvLn2N = 0x1.71547652b82fep7;   // 128 / ln2
   const double kShift = 0x1.8p52;
   const double kNegLn2HiN = -0x1.62e42fefa0000p-8;
@@ -133,7 +134,7 @@ PSM_HD double psm_exp(double x) {
   const uint64_t top = ki << 45;
   double tail;
   uint64_t sbits;
-  psm_exp_tab(idx, &tail, &sbits);
+  psm_exp_tab(tab, idx, &tail, &sbits);
   sbits += top;
   const double r2 = r * r;
   const double a = psm_fma(r, C3, C2);
@@ -146,7 +147,12 @@ PSM_HD double psm_exp(double x) {
   return psm_fma(scale, tmp, scale);
 }
 
-// The alpha argument -0.5 (u^2 + v^2) is <= 0 or NaN; psm_exp is the whole story.
-PSM_HD double psm_exp_nonpos(double x) { return psm_exp(x); }
+PSM_HD double psm_exp(double x) {
+#if defined(__CUDA_ARCH__)
+  return psm_exp_t(x, psm_exp_tab_dev);
+#else
+  return psm_exp_t(x, psm_exp_tab_host);
+#endif
+}
 
 #endif  // PSM_EXP_H
