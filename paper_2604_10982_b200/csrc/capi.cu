@@ -13,8 +13,6 @@
 // Scratch is grow-only and owned by the context (render_into's buffer reuse,
 // raster.cpp:255-262). No CPU fallback: without a CUDA device every entry
 // point returns PSM_ECUDA.
-#include <cub/cub.cuh>
-
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -38,6 +36,11 @@ struct Buf {
   size_t bytes = 0;
 };
 
+struct Planes {
+  float *color, *depth, *normal, *sem, *ins, *alpha;
+  int32_t *arg, *cnt;
+};
+
 }  // namespace psm
 
 struct psm_ctx {
@@ -52,9 +55,18 @@ struct psm_ctx {
   psm_counters last{};
   // scratch
   psm::Buf recs, bins, culls, depth_bits, tile_cnt, valid, pos, keys_c, src_c, keys_s, src_s, cnt_rank, off_rank;
-  psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, cub_tmp, dev_small, lists, rank_of, dbg_keys, topk_dbg;
+  psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
+  int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
+  int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
   psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
   int64_t* h_small = nullptr;  // pinned: counters read-back
+  // last asynchronous frame (device targets, no counters): checked, and re-rendered if it
+  // outgrew its buffers, by psm_sync
+  bool pend_valid = false;
+  const psm_scene* pend_scene = nullptr;
+  psm_camera pend_cam{};
+  psm_raster_config pend_cfg{};
+  psm::Planes pend_pl{};
 };
 
 namespace psm {
@@ -132,12 +144,11 @@ int check_config(psm_ctx* ctx, const psm_raster_config* cfg, int feat_dims) {
   return PSM_OK;
 }
 
-struct Planes {
-  float *color, *depth, *normal, *sem, *ins, *alpha;
-  int32_t *arg, *cnt;
-};
-
-// The render proper. Leaves results in `pl` (device) and counters in ctx->last.
+// The render proper: K1..K7 enqueued on the context stream with every count kept
+// on the device. The only host round trip is the first frame of a context (or a
+// frame whose RN-Total outgrew the key buffers), which reads RN-Total to size
+// them; frames after that run without a host sync. Leaves results in `pl`
+// (device) and counters in the pinned ctx->h_small (valid after the stream syncs).
 int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
                 const Planes& pl, psm_debug* dbg) {
   cudaStream_t st = ctx->stream;
@@ -165,9 +176,14 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   rs.tile_size = ts;
   rs.tiles_x = tiles_x; rs.tiles_y = tiles_y;
 
-  // small device counters: [0] err, [1] nonempty, [2] blended_total, [3] list overflow
+  // device counters (8-byte slots): [0] err, [1] nonempty tiles, [2] blended_total, [3] list overflow,
+  // [4] n_proj (u32), [5] RN-Total (u32), [6] RN kept (u32), [7] key overflow
   unsigned long long* small = nullptr;
   PSM_TRY(ensure(ctx, ctx->dev_small, 8, &small));
+  uint32_t* n_proj_dev = reinterpret_cast<uint32_t*>(small + 4);
+  uint32_t* rn_dev = reinterpret_cast<uint32_t*>(small + 5);
+  uint32_t* rn_eff_dev = reinterpret_cast<uint32_t*>(small + 6);
+  int32_t* key_ovf = reinterpret_cast<int32_t*>(small + 7);
   PSM_CUDA_TRY(cudaMemsetAsync(small, 0, 8 * sizeof(unsigned long long), st));
   int32_t* ranges = nullptr;
   PSM_TRY(ensure(ctx, ctx->ranges, static_cast<size_t>(tiles) * 2, &ranges));
@@ -175,12 +191,13 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
 
   ctx->ev_next = 0;
   record(ctx, 0);
-  int64_t n_proj = 0, rn = 0;
   uint32_t* src_s = nullptr;
   uint32_t* tvals_s = nullptr;
   uint32_t* tkeys_s = nullptr;
+  int64_t key_cap = 0;
   if (n > 0) {
-    SurfRec* recs; BinRec* bins; CullRec* culls; uint64_t* dbits; int32_t *tcnt, *valid, *pos;
+    SurfRec* recs; BinRec* bins; CullRec* culls; uint64_t* dbits; int32_t *tcnt, *valid;
+    uint32_t *pos, *scan_tmp, *hist, *totals;
     PSM_TRY(ensure(ctx, ctx->recs, n, &recs));
     PSM_TRY(ensure(ctx, ctx->bins, n, &bins));
     PSM_TRY(ensure(ctx, ctx->culls, n, &culls));
@@ -188,80 +205,66 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->tile_cnt, n, &tcnt));
     PSM_TRY(ensure(ctx, ctx->valid, n, &valid));
     PSM_TRY(ensure(ctx, ctx->pos, n, &pos));
+    PSM_TRY(ensure(ctx, ctx->scan_tmp, scan_cta_words(n) + 8, &scan_tmp));
+    PSM_TRY(ensure(ctx, ctx->hist, radix_hist_words(n), &hist));
+    PSM_TRY(ensure(ctx, ctx->totals, 256, &totals));
     launch_preprocess(sc->surfels, n, dc, rs, recs, bins, culls, dbits, tcnt, valid, reinterpret_cast<int32_t*>(small), st);
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 1);
 
-    // K2: compaction + depth sort
-    size_t tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, valid, pos, static_cast<int>(n), st);
-    void* tmp;
-    PSM_TRY(ensure(ctx, ctx->cub_tmp, tmp_bytes, reinterpret_cast<char**>(&tmp)));
-    PSM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, valid, pos, static_cast<int>(n), st));
-    int32_t tail[2];
-    PSM_CUDA_TRY(cudaMemcpyAsync(&tail[0], pos + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    PSM_CUDA_TRY(cudaMemcpyAsync(&tail[1], valid + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    int32_t err_flag = 0;
-    PSM_CUDA_TRY(cudaMemcpyAsync(&err_flag, small, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    PSM_CUDA_TRY(cudaStreamSynchronize(st));
-    if (err_flag) return fail(ctx, PSM_EINVAL, "degenerate quaternion");
-    n_proj = static_cast<int64_t>(tail[0]) + tail[1];
-    if (n_proj > 0) {
-      uint64_t *keys_c, *keys_s; uint32_t *src_c;
-      PSM_TRY(ensure(ctx, ctx->keys_c, n_proj, &keys_c));
-      PSM_TRY(ensure(ctx, ctx->src_c, n_proj, &src_c));
-      PSM_TRY(ensure(ctx, ctx->keys_s, n_proj, &keys_s));
-      PSM_TRY(ensure(ctx, ctx->src_s, n_proj, &src_s));
-      launch_compact(valid, pos, dbits, n, keys_c, src_c, st);
-      PSM_CUDA_TRY(cudaGetLastError());
-      tmp_bytes = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_c, keys_s, src_c, src_s, static_cast<int>(n_proj), 0, 63, st);
-      PSM_TRY(ensure(ctx, ctx->cub_tmp, tmp_bytes, reinterpret_cast<char**>(&tmp)));
-      PSM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_c, keys_s, src_c, src_s,
-                                                   static_cast<int>(n_proj), 0, 63, st));
-      record(ctx, 2);
+    // K2: compaction (source order kept) + stable depth sort -> rank order
+    uint64_t *keys_c, *keys_s; uint32_t *src_c;
+    PSM_TRY(ensure(ctx, ctx->keys_c, n, &keys_c));
+    PSM_TRY(ensure(ctx, ctx->src_c, n, &src_c));
+    PSM_TRY(ensure(ctx, ctx->keys_s, n, &keys_s));
+    PSM_TRY(ensure(ctx, ctx->src_s, n, &src_s));
+    exclusive_scan_i32(valid, n, pos, n_proj_dev, scan_tmp, st);
+    launch_compact(valid, reinterpret_cast<const int32_t*>(pos), dbits, n, keys_c, src_c, st);
+    bool in_alt = false;
+    radix_sort_u64(keys_c, src_c, keys_s, src_s, n_proj_dev, n, 0, 64, hist, totals, st, &in_alt);
+    PSM_CUDA_TRY(cudaGetLastError());
+    if (!in_alt) src_s = src_c;  // (8 passes: the result lands back in the first buffer)
+    record(ctx, 2);
 
-      // K3: tile counts in rank order, exclusive scan -> offsets, RN-Total
-      uint32_t *cnt_rank, *off_rank;
-      PSM_TRY(ensure(ctx, ctx->cnt_rank, n_proj, &cnt_rank));
-      PSM_TRY(ensure(ctx, ctx->off_rank, n_proj, &off_rank));
-      launch_gather_counts(src_s, tcnt, n_proj, cnt_rank, st);
-      tmp_bytes = 0;
-      cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt_rank, off_rank, static_cast<int>(n_proj), st);
-      PSM_TRY(ensure(ctx, ctx->cub_tmp, tmp_bytes, reinterpret_cast<char**>(&tmp)));
-      PSM_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt_rank, off_rank, static_cast<int>(n_proj), st));
-      uint32_t rtail[2];
-      PSM_CUDA_TRY(cudaMemcpyAsync(&rtail[0], off_rank + (n_proj - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-      PSM_CUDA_TRY(cudaMemcpyAsync(&rtail[1], cnt_rank + (n_proj - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    // K3: tile counts in rank order -> exclusive scan -> key offsets, RN-Total
+    uint32_t *cnt_rank, *off_rank;
+    PSM_TRY(ensure(ctx, ctx->cnt_rank, n, &cnt_rank));
+    PSM_TRY(ensure(ctx, ctx->off_rank, n, &off_rank));
+    launch_gather_counts(src_s, tcnt, n_proj_dev, n, cnt_rank, st);
+    exclusive_scan_u32_dev(cnt_rank, n_proj_dev, n, off_rank, rn_dev, scan_tmp, st);
+    PSM_CUDA_TRY(cudaGetLastError());
+
+    // key capacity: sized from the last frame's RN-Total; the first frame reads it (one host sync)
+    if (ctx->key_cap == 0) {
+      uint32_t rn_host = 0;
+      PSM_CUDA_TRY(cudaMemcpyAsync(&rn_host, rn_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
       PSM_CUDA_TRY(cudaStreamSynchronize(st));
-      rn = static_cast<int64_t>(rtail[0]) + rtail[1];
-      if (rn > 0x7fffffffLL) return fail(ctx, PSM_EUNSUPPORTED, "RN-Total exceeds 2^31 tile assignments");
-
-      if (rn > 0) {
-        // K4: emit (tile, source) in rank order
-        uint32_t *tkeys, *tvals, *tkeys2, *tvals2;
-        PSM_TRY(ensure(ctx, ctx->tkeys, rn, &tkeys));
-        PSM_TRY(ensure(ctx, ctx->tvals, rn, &tvals));
-        PSM_TRY(ensure(ctx, ctx->tkeys2, rn, &tkeys2));
-        PSM_TRY(ensure(ctx, ctx->tvals2, rn, &tvals2));
-        launch_emit(src_s, off_rank, n_proj, recs, bins, rs, H, tkeys, tvals, st);
-        PSM_CUDA_TRY(cudaGetLastError());
-        record(ctx, 3);
-        // K5: stable sort on the tile bits
-        tmp_bytes = 0;
-        const int tb = tile_bits(tiles);
-        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, tkeys, tkeys2, tvals, tvals2, static_cast<int>(rn), 0, tb, st);
-        PSM_TRY(ensure(ctx, ctx->cub_tmp, tmp_bytes, reinterpret_cast<char**>(&tmp)));
-        PSM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, tkeys, tkeys2, tvals, tvals2, static_cast<int>(rn),
-                                                     0, tb, st));
-        tkeys_s = tkeys2;
-        tvals_s = tvals2;
-        record(ctx, 4);
-        // K6: ranges
-        launch_ranges(tkeys_s, rn, ranges, small + 1, st);
-        PSM_CUDA_TRY(cudaGetLastError());
-      }
+      ctx->key_cap = static_cast<int64_t>(rn_host) + static_cast<int64_t>(rn_host) / 2 + 4096;
     }
+    key_cap = ctx->key_cap;
+    if (key_cap > 0x7fffffffLL) return fail(ctx, PSM_EUNSUPPORTED, "RN-Total exceeds 2^31 tile assignments");
+
+    // K4: emit (tile, source) in rank order
+    uint32_t *tkeys, *tvals, *tkeys2, *tvals2, *khist;
+    PSM_TRY(ensure(ctx, ctx->tkeys, key_cap, &tkeys));
+    PSM_TRY(ensure(ctx, ctx->tvals, key_cap, &tvals));
+    PSM_TRY(ensure(ctx, ctx->tkeys2, key_cap, &tkeys2));
+    PSM_TRY(ensure(ctx, ctx->tvals2, key_cap, &tvals2));
+    PSM_TRY(ensure(ctx, ctx->khist, radix_hist_words(key_cap), &khist));
+    launch_emit(src_s, off_rank, n_proj_dev, n, recs, bins, rs, H, tkeys, tvals, rn_dev,
+                static_cast<uint32_t>(key_cap), rn_eff_dev, key_ovf, st);
+    PSM_CUDA_TRY(cudaGetLastError());
+    record(ctx, 3);
+    // K5: stable sort on the tile bits
+    bool t_alt = false;
+    radix_sort_u32(tkeys, tvals, tkeys2, tvals2, rn_eff_dev, key_cap, 0, tile_bits(tiles), khist, totals, st, &t_alt);
+    PSM_CUDA_TRY(cudaGetLastError());
+    tkeys_s = t_alt ? tkeys2 : tkeys;
+    tvals_s = t_alt ? tvals2 : tvals;
+    record(ctx, 4);
+    // K6: ranges + non-empty tile count
+    launch_ranges(tkeys_s, rn_eff_dev, key_cap, ranges, small + 1, st);
+    PSM_CUDA_TRY(cudaGetLastError());
   }
   record(ctx, 5);
 
@@ -292,42 +295,27 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     bp.topk_dbg = tk;
   }
   const bool full_list = !topk && feat_dims > 0;
-  int cap = 0;
   if (full_list) {
-    cap = 128;
+    if (ctx->list_cap == 0) ctx->list_cap = 128;
     uint2* lists;
-    PSM_TRY(ensure(ctx, ctx->lists, npx * cap, &lists));
+    PSM_TRY(ensure(ctx, ctx->lists, npx * ctx->list_cap, &lists));
     bp.lists = lists;
-    bp.list_cap = cap;
+    bp.list_cap = ctx->list_cap;
   }
   launch_blend(bp, tiles, topk, st);
   PSM_CUDA_TRY(cudaGetLastError());
-  if (full_list) {
-    int32_t ovf = 0;
-    PSM_CUDA_TRY(cudaMemcpyAsync(&ovf, small + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    PSM_CUDA_TRY(cudaStreamSynchronize(st));
-    if (ovf > cap) {  // a pixel had more contributors than the list holds: re-run with room for all
-      cap = ovf;
-      uint2* lists;
-      PSM_TRY(ensure(ctx, ctx->lists, npx * cap, &lists));
-      bp.lists = lists;
-      bp.list_cap = cap;
-      PSM_CUDA_TRY(cudaMemsetAsync(small + 2, 0, 2 * sizeof(unsigned long long), st));
-      launch_blend(bp, tiles, topk, st);
-      PSM_CUDA_TRY(cudaGetLastError());
-    }
-  }
   record(ctx, 6);
 
-  // counters
-  PSM_CUDA_TRY(cudaMemcpyAsync(ctx->h_small, small, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  ctx->last.rn_total = static_cast<uint64_t>(rn);
-  ctx->last.n_proj = n_proj;
+  // counters -> pinned host memory (read after the stream syncs)
+  PSM_CUDA_TRY(cudaMemcpyAsync(ctx->h_small, small, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   ctx->last.tiles_x = tiles_x;
   ctx->last.tiles_y = tiles_y;
 
   if (dbg) {
     PSM_CUDA_TRY(cudaStreamSynchronize(st));
+    const unsigned long long* h = reinterpret_cast<const unsigned long long*>(ctx->h_small);
+    const int64_t n_proj = static_cast<int64_t>(static_cast<uint32_t>(h[4]));
+    const int64_t rn = static_cast<int64_t>(static_cast<uint32_t>(h[6]));
     if (dbg->tile_ranges) PSM_CUDA_TRY(cudaMemcpy(dbg->tile_ranges, ranges, sizeof(int32_t) * 2 * tiles, cudaMemcpyDeviceToHost));
     const int64_t kcopy = rn < dbg->cap_keys ? rn : dbg->cap_keys;
     if (kcopy > 0 && dbg->tile_vals) PSM_CUDA_TRY(cudaMemcpy(dbg->tile_vals, tvals_s, sizeof(int32_t) * kcopy, cudaMemcpyDeviceToHost));
@@ -336,7 +324,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
       uint64_t* dk;
       PSM_TRY(ensure(ctx, ctx->rank_of, n, &rank_of));
       PSM_TRY(ensure(ctx, ctx->dbg_keys, rn, &dk));
-      launch_rank_of(src_s, n_proj, rank_of, st);
+      launch_rank_of(src_s, n_proj_dev, n, rank_of, st);
       launch_debug_keys(tkeys_s, tvals_s, rank_of, rn, dk, st);
       PSM_CUDA_TRY(cudaGetLastError());
       PSM_CUDA_TRY(cudaMemcpyAsync(dbg->tile_keys, dk, sizeof(uint64_t) * kcopy, cudaMemcpyDeviceToHost, st));
@@ -351,10 +339,31 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   return PSM_OK;
 }
 
+// After the stream has synchronised: did the frame fit its buffers? Grows them if not
+// (the caller then re-renders). Also raises PSM_EINVAL for a degenerate quaternion.
+int check_frame(psm_ctx* ctx, bool* rerun) {
+  const unsigned long long* h = reinterpret_cast<const unsigned long long*>(ctx->h_small);
+  *rerun = false;
+  if (static_cast<int32_t>(h[0])) return fail(ctx, PSM_EINVAL, "degenerate quaternion");
+  const uint32_t rn = static_cast<uint32_t>(h[5]);
+  if (static_cast<int32_t>(h[7])) {  // RN-Total outgrew the key buffers
+    ctx->key_cap = static_cast<int64_t>(rn) + static_cast<int64_t>(rn) / 2 + 4096;
+    *rerun = true;
+  }
+  const int32_t m = static_cast<int32_t>(h[3]);
+  if (m > ctx->list_cap && ctx->list_cap > 0) {  // a pixel had more contributors than the Full-mode list holds
+    ctx->list_cap = m;
+    *rerun = true;
+  }
+  return PSM_OK;
+}
+
 void finish_counters(psm_ctx* ctx) {
   const unsigned long long* h = reinterpret_cast<const unsigned long long*>(ctx->h_small);
   ctx->last.nonempty_tiles = static_cast<int64_t>(h[1]);
   ctx->last.blended_total = h[2];
+  ctx->last.n_proj = static_cast<int64_t>(static_cast<uint32_t>(h[4]));
+  ctx->last.rn_total = static_cast<uint64_t>(static_cast<uint32_t>(h[5]));
   ctx->last.rn_per_tile = h[1] > 0 ? static_cast<double>(ctx->last.rn_total) / static_cast<double>(h[1]) : 0.0;
 }
 
@@ -405,8 +414,8 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
     if (!tg->sem_feat) pl.sem = nullptr;
     if (!tg->ins_dist) pl.ins = nullptr;
   }
-  PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg));
-  if (!tg->on_device) {
+  auto enqueue_d2h = [&]() -> int {
+    if (tg->on_device) return PSM_OK;
     cudaStream_t st = ctx->stream;
     auto d2h = [&](void* dst, const void* src, size_t bytes) -> int {
       if (dst) PSM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
@@ -420,13 +429,51 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
     PSM_TRY(d2h(tg->blend_count, pl.cnt, npx * 4));
     if (pl.sem) PSM_TRY(d2h(tg->sem_feat, pl.sem, npx * cs * 4));
     if (pl.ins) PSM_TRY(d2h(tg->ins_dist, pl.ins, npx * nq * 4));
-  }
-  if (counters || !tg->on_device || ctx->profiling) {
-    PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return PSM_OK;
+  };
+  PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg));
+  PSM_TRY(enqueue_d2h());
+  if (counters || !tg->on_device || ctx->profiling || dbg) {
+    for (int attempt = 0;; ++attempt) {
+      PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      bool rerun = false;
+      PSM_TRY(check_frame(ctx, &rerun));
+      if (!rerun) break;
+      if (attempt >= 3) return fail(ctx, PSM_ENOMEM, "render buffers did not converge");
+      PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg));
+      PSM_TRY(enqueue_d2h());
+    }
+    ctx->pend_valid = false;
     finish_counters(ctx);
     read_times(ctx);
     if (counters) *counters = ctx->last;
+  } else {
+    ctx->pend_valid = true;
+    ctx->pend_scene = sc;
+    ctx->pend_cam = *cam;
+    ctx->pend_cfg = *cfg;
+    ctx->pend_pl = pl;
   }
+  return PSM_OK;
+}
+
+// psm_sync: wait, validate the last asynchronous frame, re-render it if it outgrew its buffers.
+int sync_impl(psm_ctx* ctx) {
+  PSM_CUDA_TRY(cudaSetDevice(ctx->device));
+  PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (ctx->pend_valid) {
+    for (int attempt = 0;; ++attempt) {
+      bool rerun = false;
+      PSM_TRY(check_frame(ctx, &rerun));
+      if (!rerun) break;
+      if (attempt >= 3) return fail(ctx, PSM_ENOMEM, "render buffers did not converge");
+      PSM_TRY(render_impl(ctx, ctx->pend_scene, &ctx->pend_cam, &ctx->pend_cfg, ctx->pend_pl, nullptr));
+      PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+    ctx->pend_valid = false;
+  }
+  finish_counters(ctx);
+  read_times(ctx);
   return PSM_OK;
 }
 
@@ -468,7 +515,7 @@ int psm_destroy(psm_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->culls, &ctx->depth_bits, &ctx->tile_cnt, &ctx->valid, &ctx->pos,
                       &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s, &ctx->cnt_rank, &ctx->off_rank,
-                      &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->cub_tmp,
+                      &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
                       &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,
                       &ctx->plane_color, &ctx->plane_depth, &ctx->plane_normal, &ctx->plane_sem, &ctx->plane_ins,
                       &ctx->plane_arg, &ctx->plane_alpha, &ctx->plane_cnt};
@@ -496,11 +543,7 @@ int psm_get_stage_times(const psm_ctx* ctx, psm_stage_times* out) {
 
 int psm_sync(psm_ctx* ctx) {
   if (!ctx) return PSM_EINVAL;
-  cudaError_t e = cudaStreamSynchronize(ctx->stream);
-  if (e != cudaSuccess) return psm::fail_cuda(ctx, e, "cudaStreamSynchronize", __FILE__, __LINE__);
-  psm::finish_counters(ctx);
-  psm::read_times(ctx);
-  return PSM_OK;
+  return psm::sync_impl(ctx);
 }
 
 int psm_last_counters(const psm_ctx* ctx, psm_counters* out) {

@@ -37,16 +37,34 @@ void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam,
 // binning.cu
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n,
                     uint64_t* keys_out, uint32_t* src_out, cudaStream_t st);
-void launch_gather_counts(const uint32_t* src_by_rank, const int32_t* tile_cnt, int64_t n_proj, uint32_t* cnt_by_rank,
-                          cudaStream_t st);
-void launch_emit(const uint32_t* src_by_rank, const uint32_t* offsets, int64_t n_proj, const SurfRec* recs,
-                 const BinRec* bins, const DevRaster& rs, int img_h, uint32_t* tile_keys, uint32_t* tile_vals,
+void launch_gather_counts(const uint32_t* src_by_rank, const int32_t* tile_cnt, const uint32_t* n_proj_dev, int64_t cap,
+                          uint32_t* cnt_by_rank, cudaStream_t st);
+void launch_emit(const uint32_t* src_by_rank, const uint32_t* offsets, const uint32_t* n_proj_dev, int64_t cap_proj,
+                 const SurfRec* recs, const BinRec* bins, const DevRaster& rs, int img_h, uint32_t* tile_keys,
+                 uint32_t* tile_vals, const uint32_t* rn_dev, uint32_t cap_keys, uint32_t* rn_eff, int32_t* overflow,
                  cudaStream_t st);
-void launch_ranges(const uint32_t* sorted_tiles, int64_t rn, int32_t* ranges, unsigned long long* nonempty,
-                   cudaStream_t st);
-void launch_rank_of(const uint32_t* src_by_rank, int64_t n_proj, int32_t* rank_of, cudaStream_t st);
+void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* rn_dev, int64_t cap, int32_t* ranges,
+                   unsigned long long* nonempty, cudaStream_t st);
+void launch_rank_of(const uint32_t* src_by_rank, const uint32_t* n_proj_dev, int64_t cap, int32_t* rank_of,
+                    cudaStream_t st);
 void launch_debug_keys(const uint32_t* sorted_tiles, const uint32_t* sorted_vals, const int32_t* rank_of, int64_t rn,
                        uint64_t* keys_out, cudaStream_t st);
+
+// scan.cu
+size_t scan_cta_words(int64_t cap);
+void exclusive_scan_i32(const int32_t* in, int64_t n, uint32_t* out, uint32_t* total_dev, uint32_t* cta_sums,
+                        cudaStream_t st);
+void exclusive_scan_u32_dev(const uint32_t* in, const uint32_t* n_dev, int64_t cap, uint32_t* out, uint32_t* total_dev,
+                            uint32_t* cta_sums, cudaStream_t st);
+
+// radix_sort.cu
+size_t radix_hist_words(int64_t cap);
+void radix_sort_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
+                    int64_t cap, int begin_bit, int end_bit, uint32_t* hist, uint32_t* totals, cudaStream_t st,
+                    bool* result_in_alt);
+void radix_sort_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
+                    int64_t cap, int begin_bit, int end_bit, uint32_t* hist, uint32_t* totals, cudaStream_t st,
+                    bool* result_in_alt);
 
 // blend.cu
 int blend_kmax_for(int k_sel);
