@@ -302,9 +302,8 @@ def run_ours(args):
                      "peak_source": peak_src, "alg_bytes_per_launch": b_blend, "launch_ms": blend_avg},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 6 * args.steps,
-        "gpu_launches_note": "our kernels per step: preprocess, compact, gather_counts, emit, ranges, blend "
-                             "(+ CUB radix sorts / scans)",
+        "gpu_launches": 5 * args.steps,
+        "gpu_launches_note": "per step: preprocess, tile_scan, emit, sort_tiles, blend (+2 memsets)",
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -108,7 +108,8 @@ typedef struct psm_counters {
 } psm_counters;
 
 /* Debug export for the parity suite (host pointers, caller-owned; any may be NULL).
- *   tile_keys   [cap_keys] sorted (tile << 32 | depth rank) keys
+ *   tile_keys   [cap_keys] sorted (tile << 32 | depth rank) keys, rank = position of the
+ *               surfel in the (sort_depth, source) order of all projected surfels
  *   tile_vals   [cap_keys] source surfel index of each key (the tile lists of
  *               TileGrid::tiles, raster.hpp:35, as scene indices)
  *   tile_ranges [2 * tiles] [start, end) of each tile in tile_keys
@@ -130,11 +131,10 @@ typedef struct psm_debug {
 /* Stage timings of the last render when profiling is on (CUDA events on the
  * context stream), milliseconds. */
 typedef struct psm_stage_times {
-  float preprocess;   /* K1: project_surfel + hot-record build (raster.cpp:94-142,321-353) */
-  float depth_sort;   /* K2: (sort_depth, source) order (raster.cpp:78-83) */
-  float emit;         /* K3/K4: per-surfel tile counts, scan, key emission (raster.cpp:59-74) */
-  float tile_sort;    /* K5: stable sort by tile */
-  float ranges;       /* K6: per-tile [start,end) + counters (raster.cpp:84-88) */
+  float preprocess;   /* K1: project_surfel, hot records, box, per-tile bucket sizes (raster.cpp:94-142,321-353,59-74) */
+  float tile_scan;    /* K3: bucket offsets = per-tile ranges, RN-Total (raster.cpp:84-88) */
+  float emit;         /* K4: (tile, surfel) pairs into their buckets (raster.cpp:69-73) */
+  float tile_sort;    /* K5: per-tile sort by (sort_depth, source) (raster.cpp:77-83) */
   float blend;        /* K7: per-pixel compositing + Top-K + features (raster.cpp:355-506) */
   float total;
 } psm_stage_times;

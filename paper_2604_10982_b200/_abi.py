@@ -48,8 +48,8 @@ class psm_debug(C.Structure):
 
 
 class psm_stage_times(C.Structure):
-    _fields_ = [("preprocess", C.c_float), ("depth_sort", C.c_float), ("emit", C.c_float), ("tile_sort", C.c_float),
-                ("ranges", C.c_float), ("blend", C.c_float), ("total", C.c_float)]
+    _fields_ = [("preprocess", C.c_float), ("tile_scan", C.c_float), ("emit", C.c_float), ("tile_sort", C.c_float),
+                ("blend", C.c_float), ("total", C.c_float)]
 
     def as_dict(self):
         return {k: float(getattr(self, k)) for k, _ in self._fields_}

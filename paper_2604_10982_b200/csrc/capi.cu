@@ -54,7 +54,7 @@ struct psm_ctx {
   psm_stage_times times{};
   psm_counters last{};
   // scratch
-  psm::Buf recs, bins, culls, depth_bits, tile_cnt, valid, pos, keys_c, src_c, keys_s, src_s, cnt_rank, off_rank;
+  psm::Buf recs, bins, culls, depth_bits, tile_counts, cursor, tile_totals, tile_start, kscratch, valid, pos, keys_c, src_c, keys_s, src_s;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
@@ -125,7 +125,7 @@ int tile_bits(int tiles) {
   return b;
 }
 
-// Stage boundary i (0..6); boundaries of skipped stages are recorded at the
+// Stage boundary i (0..5); boundaries of skipped stages are recorded at the
 // same point so they time as zero.
 void record(psm_ctx* ctx, int i) {
   if (!ctx->profiling) return;
@@ -191,51 +191,31 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
 
   ctx->ev_next = 0;
   record(ctx, 0);
-  uint32_t* src_s = nullptr;
   uint32_t* tvals_s = nullptr;
-  uint32_t* tkeys_s = nullptr;
   int64_t key_cap = 0;
   if (n > 0) {
-    SurfRec* recs; BinRec* bins; CullRec* culls; uint64_t* dbits; int32_t *tcnt, *valid;
-    uint32_t *pos, *scan_tmp, *hist, *totals;
+    SurfRec* recs; BinRec* bins; CullRec* culls; uint64_t* dbits; int32_t* valid;
+    uint32_t *tcounts, *cursor, *ttotals, *tstart;
     PSM_TRY(ensure(ctx, ctx->recs, n, &recs));
     PSM_TRY(ensure(ctx, ctx->bins, n, &bins));
     PSM_TRY(ensure(ctx, ctx->culls, n, &culls));
     PSM_TRY(ensure(ctx, ctx->depth_bits, n, &dbits));
-    PSM_TRY(ensure(ctx, ctx->tile_cnt, n, &tcnt));
     PSM_TRY(ensure(ctx, ctx->valid, n, &valid));
-    PSM_TRY(ensure(ctx, ctx->pos, n, &pos));
-    PSM_TRY(ensure(ctx, ctx->scan_tmp, scan_cta_words(n) + 8, &scan_tmp));
-    PSM_TRY(ensure(ctx, ctx->hist, radix_hist_words(n), &hist));
-    PSM_TRY(ensure(ctx, ctx->totals, 256, &totals));
-    launch_preprocess(sc->surfels, n, dc, rs, recs, bins, culls, dbits, tcnt, valid, reinterpret_cast<int32_t*>(small), st);
+    PSM_TRY(ensure(ctx, ctx->tile_counts, static_cast<size_t>(tiles) * kSplit, &tcounts));
+    PSM_TRY(ensure(ctx, ctx->cursor, static_cast<size_t>(tiles) * kSplit, &cursor));
+    PSM_TRY(ensure(ctx, ctx->tile_totals, tiles, &ttotals));
+    PSM_TRY(ensure(ctx, ctx->tile_start, tiles, &tstart));
+    PSM_CUDA_TRY(cudaMemsetAsync(tcounts, 0, sizeof(uint32_t) * tiles * kSplit, st));
+    // K1: projection, records, per-tile bucket sizes
+    launch_preprocess(sc->surfels, n, dc, rs, recs, bins, culls, dbits, tcounts, valid, n_proj_dev,
+                      reinterpret_cast<int32_t*>(small), st);
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 1);
 
-    // K2: compaction (source order kept) + stable depth sort -> rank order
-    uint64_t *keys_c, *keys_s; uint32_t *src_c;
-    PSM_TRY(ensure(ctx, ctx->keys_c, n, &keys_c));
-    PSM_TRY(ensure(ctx, ctx->src_c, n, &src_c));
-    PSM_TRY(ensure(ctx, ctx->keys_s, n, &keys_s));
-    PSM_TRY(ensure(ctx, ctx->src_s, n, &src_s));
-    exclusive_scan_i32(valid, n, pos, n_proj_dev, scan_tmp, st);
-    launch_compact(valid, reinterpret_cast<const int32_t*>(pos), dbits, n, keys_c, src_c, st);
-    bool in_alt = false;
-    radix_sort_u64(keys_c, src_c, keys_s, src_s, n_proj_dev, n, 0, 64, hist, totals, st, &in_alt);
-    PSM_CUDA_TRY(cudaGetLastError());
-    if (!in_alt) src_s = src_c;  // (8 passes: the result lands back in the first buffer)
-    record(ctx, 2);
-
-    // K3: tile counts in rank order -> exclusive scan -> key offsets, RN-Total
-    uint32_t *cnt_rank, *off_rank;
-    PSM_TRY(ensure(ctx, ctx->cnt_rank, n, &cnt_rank));
-    PSM_TRY(ensure(ctx, ctx->off_rank, n, &off_rank));
-    launch_gather_counts(src_s, tcnt, n_proj_dev, n, cnt_rank, st);
-    exclusive_scan_u32_dev(cnt_rank, n_proj_dev, n, off_rank, rn_dev, scan_tmp, st);
-    PSM_CUDA_TRY(cudaGetLastError());
-
     // key capacity: sized from the last frame's RN-Total; the first frame reads it (one host sync)
     if (ctx->key_cap == 0) {
+      launch_tile_scan(tcounts, tiles, 0xffffffffu, ranges, cursor, ttotals, tstart, rn_dev, rn_eff_dev, small + 1,
+                       key_ovf, st);
       uint32_t rn_host = 0;
       PSM_CUDA_TRY(cudaMemcpyAsync(&rn_host, rn_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
       PSM_CUDA_TRY(cudaStreamSynchronize(st));
@@ -243,31 +223,26 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     }
     key_cap = ctx->key_cap;
     if (key_cap > 0x7fffffffLL) return fail(ctx, PSM_EUNSUPPORTED, "RN-Total exceeds 2^31 tile assignments");
-
-    // K4: emit (tile, source) in rank order
-    uint32_t *tkeys, *tvals, *tkeys2, *tvals2, *khist;
-    PSM_TRY(ensure(ctx, ctx->tkeys, key_cap, &tkeys));
+    uint32_t* tvals;
+    uint64_t* kscratch;
     PSM_TRY(ensure(ctx, ctx->tvals, key_cap, &tvals));
-    PSM_TRY(ensure(ctx, ctx->tkeys2, key_cap, &tkeys2));
-    PSM_TRY(ensure(ctx, ctx->tvals2, key_cap, &tvals2));
-    PSM_TRY(ensure(ctx, ctx->khist, radix_hist_words(key_cap), &khist));
-    launch_emit(src_s, off_rank, n_proj_dev, n, recs, bins, rs, H, tkeys, tvals, rn_dev,
-                static_cast<uint32_t>(key_cap), rn_eff_dev, key_ovf, st);
+    PSM_TRY(ensure(ctx, ctx->kscratch, key_cap, &kscratch));
+
+    // K3: bucket offsets = per-tile ranges, RN-Total, non-empty tiles
+    launch_tile_scan(tcounts, tiles, static_cast<uint32_t>(key_cap), ranges, cursor, ttotals, tstart, rn_dev,
+                     rn_eff_dev, small + 1, key_ovf, st);
+    PSM_CUDA_TRY(cudaGetLastError());
+    record(ctx, 2);
+    // K4: every (surfel, tile) pair into its tile's bucket
+    launch_emit(valid, n, recs, bins, rs, H, cursor, tstart, static_cast<uint32_t>(key_cap), tvals, st);
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 3);
-    // K5: stable sort on the tile bits
-    bool t_alt = false;
-    radix_sort_u32(tkeys, tvals, tkeys2, tvals2, rn_eff_dev, key_cap, 0, tile_bits(tiles), khist, totals, st, &t_alt);
+    // K5: per-tile sort by (depth bits, source)
+    launch_sort_tiles(ranges, tiles, dbits, tvals, kscratch, st);
     PSM_CUDA_TRY(cudaGetLastError());
-    tkeys_s = t_alt ? tkeys2 : tkeys;
-    tvals_s = t_alt ? tvals2 : tvals;
+    tvals_s = tvals;
     record(ctx, 4);
-    // K6: ranges + non-empty tile count
-    launch_ranges(tkeys_s, rn_eff_dev, key_cap, ranges, small + 1, st);
-    PSM_CUDA_TRY(cudaGetLastError());
   }
-  record(ctx, 5);
-
   // K7: blend
   BlendParams bp;
   std::memset(&bp, 0, sizeof bp);
@@ -304,7 +279,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   }
   launch_blend(bp, tiles, topk, st);
   PSM_CUDA_TRY(cudaGetLastError());
-  record(ctx, 6);
+  record(ctx, 5);
 
   // counters -> pinned host memory (read after the stream syncs)
   PSM_CUDA_TRY(cudaMemcpyAsync(ctx->h_small, small, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -319,19 +294,38 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     if (dbg->tile_ranges) PSM_CUDA_TRY(cudaMemcpy(dbg->tile_ranges, ranges, sizeof(int32_t) * 2 * tiles, cudaMemcpyDeviceToHost));
     const int64_t kcopy = rn < dbg->cap_keys ? rn : dbg->cap_keys;
     if (kcopy > 0 && dbg->tile_vals) PSM_CUDA_TRY(cudaMemcpy(dbg->tile_vals, tvals_s, sizeof(int32_t) * kcopy, cudaMemcpyDeviceToHost));
-    if (kcopy > 0 && dbg->tile_keys) {
+    if ((kcopy > 0 && dbg->tile_keys) || dbg->depth_order) {
+      // debug only: the global depth rank of every projected surfel ((sort_depth, source)
+      // order), by compaction + the stable radix sort, for the (tile << 32 | rank) keys
       int32_t* rank_of;
-      uint64_t* dk;
+      uint64_t *dk, *keys_c, *keys_s;
+      uint32_t *pos, *src_c, *src_s, *scan_tmp, *hist, *totals;
       PSM_TRY(ensure(ctx, ctx->rank_of, n, &rank_of));
-      PSM_TRY(ensure(ctx, ctx->dbg_keys, rn, &dk));
-      launch_rank_of(src_s, n_proj_dev, n, rank_of, st);
-      launch_debug_keys(tkeys_s, tvals_s, rank_of, rn, dk, st);
+      PSM_TRY(ensure(ctx, ctx->dbg_keys, rn > 0 ? rn : 1, &dk));
+      PSM_TRY(ensure(ctx, ctx->keys_c, n, &keys_c));
+      PSM_TRY(ensure(ctx, ctx->keys_s, n, &keys_s));
+      PSM_TRY(ensure(ctx, ctx->pos, n, &pos));
+      PSM_TRY(ensure(ctx, ctx->src_c, n, &src_c));
+      PSM_TRY(ensure(ctx, ctx->src_s, n, &src_s));
+      PSM_TRY(ensure(ctx, ctx->scan_tmp, scan_cta_words(n) + 8, &scan_tmp));
+      PSM_TRY(ensure(ctx, ctx->hist, radix_hist_words(n), &hist));
+      PSM_TRY(ensure(ctx, ctx->totals, 256, &totals));
+      const int32_t* valid = static_cast<const int32_t*>(ctx->valid.p);
+      const uint64_t* dbits = static_cast<const uint64_t*>(ctx->depth_bits.p);
+      exclusive_scan_i32(valid, n, pos, totals + 255, scan_tmp, st);
+      launch_compact(valid, reinterpret_cast<const int32_t*>(pos), dbits, n, keys_c, src_c, st);
+      bool in_alt = false;
+      radix_sort_u64(keys_c, src_c, keys_s, src_s, n_proj_dev, n, 0, 64, hist, totals, st, &in_alt);
+      const uint32_t* order = in_alt ? src_s : src_c;
+      launch_rank_of(order, n_proj_dev, n, rank_of, st);
+      launch_debug_keys(ranges, tiles, tvals_s, rank_of, dk, st);
       PSM_CUDA_TRY(cudaGetLastError());
-      PSM_CUDA_TRY(cudaMemcpyAsync(dbg->tile_keys, dk, sizeof(uint64_t) * kcopy, cudaMemcpyDeviceToHost, st));
+      if (kcopy > 0 && dbg->tile_keys)
+        PSM_CUDA_TRY(cudaMemcpyAsync(dbg->tile_keys, dk, sizeof(uint64_t) * kcopy, cudaMemcpyDeviceToHost, st));
+      const int64_t pcopy = n_proj < dbg->cap_proj ? n_proj : dbg->cap_proj;
+      if (pcopy > 0 && dbg->depth_order)
+        PSM_CUDA_TRY(cudaMemcpyAsync(dbg->depth_order, order, sizeof(int32_t) * pcopy, cudaMemcpyDeviceToHost, st));
     }
-    const int64_t pcopy = n_proj < dbg->cap_proj ? n_proj : dbg->cap_proj;
-    if (pcopy > 0 && dbg->depth_order)
-      PSM_CUDA_TRY(cudaMemcpyAsync(dbg->depth_order, src_s, sizeof(int32_t) * pcopy, cudaMemcpyDeviceToHost, st));
     if (bp.topk_dbg)
       PSM_CUDA_TRY(cudaMemcpyAsync(dbg->topk_src, bp.topk_dbg, sizeof(int32_t) * npx * k_sel, cudaMemcpyDeviceToHost, st));
     PSM_CUDA_TRY(cudaStreamSynchronize(st));
@@ -368,16 +362,15 @@ void finish_counters(psm_ctx* ctx) {
 }
 
 void read_times(psm_ctx* ctx) {
-  if (!ctx->profiling) return;
-  float t[6] = {};
-  for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&t[i], ctx->ev[i], ctx->ev[i + 1]);
+  if (!ctx->profiling || ctx->ev_next < 6) return;
+  float t[5] = {};
+  for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], ctx->ev[i], ctx->ev[i + 1]);
   ctx->times.preprocess = t[0];
-  ctx->times.depth_sort = t[1];
+  ctx->times.tile_scan = t[1];
   ctx->times.emit = t[2];
   ctx->times.tile_sort = t[3];
-  ctx->times.ranges = t[4];
-  ctx->times.blend = t[5];
-  cudaEventElapsedTime(&ctx->times.total, ctx->ev[0], ctx->ev[6]);
+  ctx->times.blend = t[4];
+  cudaEventElapsedTime(&ctx->times.total, ctx->ev[0], ctx->ev[5]);
 }
 
 int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
@@ -513,8 +506,8 @@ int psm_destroy(psm_ctx* ctx) {
   if (!ctx) return PSM_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->culls, &ctx->depth_bits, &ctx->tile_cnt, &ctx->valid, &ctx->pos,
-                      &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s, &ctx->cnt_rank, &ctx->off_rank,
+  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->culls, &ctx->depth_bits, &ctx->tile_counts, &ctx->cursor, &ctx->tile_totals, &ctx->tile_start, &ctx->kscratch, &ctx->valid, &ctx->pos,
+                      &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s,
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
                       &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,
                       &ctx->plane_color, &ctx->plane_depth, &ctx->plane_normal, &ctx->plane_sem, &ctx->plane_ins,

@@ -15,31 +15,36 @@ namespace {
 
 __device__ __forceinline__ double sum3(double a, double b, double c) { return (a + b) + c; }
 
-// Tile count of one surfel under the active binning (bin_boxes, raster.cpp:59-74;
-// Ellipse extension in psm_ellipse.h).
-__device__ __forceinline__ int tile_count(const BinRec& b, double cx, double cy, const DevRaster& rs, int img_h) {
-  if (b.tx0 > b.tx1 || b.ty0 > b.ty1) return 0;
-  if (rs.binning != PSM_BIN_ELLIPSE) return (b.tx1 - b.tx0 + 1) * (b.ty1 - b.ty0 + 1);
-  int total = 0;
+// Adds one to the counter of every tile the surfel is binned to (bin_boxes,
+// raster.cpp:59-74; Ellipse extension in psm_ellipse.h): the per-tile bucket sizes
+// of the counting sort that replaces the reference's per-tile push_back. Each tile
+// has kSplit sub-counters (sub-bucket = lane), laid out split-major, so the atomics
+// of a hot tile (10k entries near the camera) spread over kSplit addresses.
+__device__ __forceinline__ void count_tiles(const BinRec& b, double cx, double cy, const DevRaster& rs, int img_h,
+                                            uint32_t* __restrict__ tile_counts) {
+  if (b.tx0 > b.tx1 || b.ty0 > b.ty1) return;
   for (int ty = b.ty0; ty <= b.ty1; ++ty) {
-    int lo, hi;
-    if (psm_ellipse_row(cx, cy, b.F00, b.F01, b.F11, rs.chi2, ty, rs.tile_size, img_h, b.tx0, b.tx1, &lo, &hi))
-      total += hi - lo + 1;
+    int lo = b.tx0, hi = b.tx1;
+    if (rs.binning == PSM_BIN_ELLIPSE &&
+        !psm_ellipse_row(cx, cy, b.F00, b.F01, b.F11, rs.chi2, ty, rs.tile_size, img_h, b.tx0, b.tx1, &lo, &hi))
+      continue;
+    uint32_t* row = tile_counts + static_cast<int64_t>(threadIdx.x & (kSplit - 1)) * rs.tiles_x * rs.tiles_y +
+                    ty * rs.tiles_x;
+    for (int tx = lo; tx <= hi; ++tx) atomicAdd(row + tx, 1u);
   }
-  return total;
 }
 
 __global__ void __launch_bounds__(256) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
                                                           DevCamera cam, DevRaster rs, SurfRec* __restrict__ recs,
                                                           BinRec* __restrict__ bins, CullRec* __restrict__ culls,
                                                           uint64_t* __restrict__ depth_bits,
-                                                          int32_t* __restrict__ tile_cnt, int32_t* __restrict__ valid,
+                                                          uint32_t* __restrict__ tile_counts,
+                                                          int32_t* __restrict__ valid, uint32_t* __restrict__ n_proj,
                                                           int32_t* __restrict__ err) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double* s = surfels13 + 13 * i;
   valid[i] = 0;
-  tile_cnt[i] = 0;
 
   // p_cam = r_cw * mu + t_cw (Camera::to_camera, core_types.hpp:51)
   const double mu0 = s[0], mu1 = s[1], mu2 = s[2];
@@ -181,19 +186,23 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const double* __restric
     culls[i] = c;
   }
   depth_bits[i] = static_cast<uint64_t>(__double_as_longlong(zz));
-  tile_cnt[i] = tile_count(b, cx, cy, rs, cam.h);
+  count_tiles(b, cx, cy, rs, cam.h, tile_counts);
   valid[i] = 1;
+  {  // n_proj: one atomic per warp
+    const unsigned m = __activemask();
+    if ((threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(n_proj, static_cast<uint32_t>(__popc(m)));
+  }
 }
 
 }  // namespace
 
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
-                       BinRec* bins, CullRec* culls, uint64_t* depth_bits, int32_t* tile_cnt, int32_t* valid,
-                       int32_t* err, cudaStream_t stream) {
+                       BinRec* bins, CullRec* culls, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,
+                       uint32_t* n_proj, int32_t* err, cudaStream_t stream) {
   if (n <= 0) return;
   const int64_t blocks = (n + 255) / 256;
   preprocess_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(surfels13, n, cam, rs, recs, bins, culls, depth_bits,
-                                                                       tile_cnt, valid, err);
+                                                                       tile_counts, valid, n_proj, err);
 }
 
 }  // namespace psm

@@ -51,6 +51,9 @@ struct __align__(16) CullRec {
 };
 static_assert(sizeof(CullRec) == 32, "CullRec must be 32 bytes");
 
+// Sub-buckets per tile for the counting sort's atomics (binning.cu).
+constexpr int kSplit = 32;
+
 // Camera by value in kernel parameters.
 struct DevCamera {
   double r[9];  // column-major r_cw

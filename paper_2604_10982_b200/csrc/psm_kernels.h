@@ -31,23 +31,23 @@ struct BlendParams {
 
 // K1 preprocess.cu
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
-                       BinRec* bins, CullRec* culls, uint64_t* depth_bits, int32_t* tile_cnt, int32_t* valid,
-                       int32_t* err, cudaStream_t stream);
+                       BinRec* bins, CullRec* culls, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,
+                       uint32_t* n_proj, int32_t* err, cudaStream_t stream);
 
 // binning.cu
+void launch_tile_scan(const uint32_t* tile_counts, int tiles, uint32_t cap, int32_t* ranges, uint32_t* cursor,
+                      uint32_t* totals, uint32_t* tile_start, uint32_t* rn_dev, uint32_t* rn_eff,
+                      unsigned long long* nonempty, int32_t* overflow, cudaStream_t st);
+void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const BinRec* bins, const DevRaster& rs,
+                 int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint32_t* tile_vals,
+                 cudaStream_t st);
+void launch_sort_tiles(const int32_t* ranges, int tiles, const uint64_t* depth_bits, uint32_t* tile_vals,
+                       uint64_t* key_scratch, cudaStream_t st);
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n,
                     uint64_t* keys_out, uint32_t* src_out, cudaStream_t st);
-void launch_gather_counts(const uint32_t* src_by_rank, const int32_t* tile_cnt, const uint32_t* n_proj_dev, int64_t cap,
-                          uint32_t* cnt_by_rank, cudaStream_t st);
-void launch_emit(const uint32_t* src_by_rank, const uint32_t* offsets, const uint32_t* n_proj_dev, int64_t cap_proj,
-                 const SurfRec* recs, const BinRec* bins, const DevRaster& rs, int img_h, uint32_t* tile_keys,
-                 uint32_t* tile_vals, const uint32_t* rn_dev, uint32_t cap_keys, uint32_t* rn_eff, int32_t* overflow,
-                 cudaStream_t st);
-void launch_ranges(const uint32_t* sorted_tiles, const uint32_t* rn_dev, int64_t cap, int32_t* ranges,
-                   unsigned long long* nonempty, cudaStream_t st);
 void launch_rank_of(const uint32_t* src_by_rank, const uint32_t* n_proj_dev, int64_t cap, int32_t* rank_of,
                     cudaStream_t st);
-void launch_debug_keys(const uint32_t* sorted_tiles, const uint32_t* sorted_vals, const int32_t* rank_of, int64_t rn,
+void launch_debug_keys(const int32_t* ranges, int tiles, const uint32_t* sorted_vals, const int32_t* rank_of,
                        uint64_t* keys_out, cudaStream_t st);
 
 // scan.cu
