@@ -10,11 +10,11 @@
 //   K4 emit        every (surfel, tile) pair claims a slot of its tile's bucket
 //                  (atomic cursor; order inside a bucket is arbitrary)
 //   K5 sort_tiles  one CTA per tile sorts its bucket by the total order
-//                  (fp64 depth bits, source) with a bitonic network in shared
-//                  memory (flip formulation, implicit +inf padding), so the
-//                  result is the reference's list whatever order K4 produced.
-//                  Buckets larger than 4096 entries fall back to the same network
-//                  over global memory.
+//                  (fp64 depth bits, source), packed into one 64-bit key, with a
+//                  bitonic network held in registers (shuffles within a warp,
+//                  shared memory beyond), so the result is the reference's list
+//                  whatever order K4 produced. Size classes: <= 4096 entries
+//                  (256 threads), <= 16384 (1024 threads), larger over global memory.
 // Every count stays on the device; key buffers are capacity-checked (the host
 // re-renders a frame whose RN-Total outgrew them, capi.cu).
 #include "psm_device.cuh"
@@ -103,13 +103,35 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
   }
 }
 
+// ---------------------------------------------------------------- K5 per-tile sort
+// Sort key of a (surfel, tile) entry: the reference's per-tile order is
+// (sort_depth, source) (raster.cpp:78-83); positive fp64 depths order as their bit
+// patterns, so key = ((bits - min_bits) >> sh) << src_bits | source orders exactly
+// like (depth, source) whenever sh = 0, and up to ties of the dropped low depth
+// bits otherwise (fixed up after the sort). min_bits / max_bits are the frame's
+// extreme depth bit patterns (K1), sh = max(0, bitlen(max - min) + src_bits - 64).
+__device__ __forceinline__ int key_shift(const unsigned long long* __restrict__ depth_minmax, int src_bits) {
+  const uint64_t range = depth_minmax[1] - depth_minmax[0];
+  const int len = range ? 64 - __clzll(static_cast<long long>(range)) : 0;
+  const int sh = len + src_bits - 64;
+  return sh > 0 ? sh : 0;
+}
+
+__device__ __forceinline__ uint64_t sort_key(uint64_t bits, uint32_t src, uint64_t min_bits, int sh, int src_bits) {
+  return (((bits - min_bits) >> sh) << src_bits) | src;
+}
+
 __global__ void __launch_bounds__(256) emit_kernel(const int32_t* __restrict__ valid, int64_t n,
                                                    const SurfRec* __restrict__ recs, const BinRec* __restrict__ bins,
                                                    DevRaster rs, int img_h, uint32_t* __restrict__ cursor,
                                                    const uint32_t* __restrict__ tile_start, uint32_t cap,
-                                                   uint32_t* __restrict__ tile_vals) {
+                                                   uint64_t* __restrict__ tile_keys,
+                                                   const uint64_t* __restrict__ depth_bits,
+                                                   const unsigned long long* __restrict__ depth_minmax, int src_bits) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n || !valid[i]) return;
+  const uint64_t key = sort_key(depth_bits[i], static_cast<uint32_t>(i), depth_minmax[0],
+                                key_shift(depth_minmax, src_bits), src_bits);
   const BinRec b = bins[i];
   if (b.tx0 > b.tx1 || b.ty0 > b.ty1) return;
   const bool ellipse = rs.binning == PSM_BIN_ELLIPSE;
@@ -122,79 +144,207 @@ __global__ void __launch_bounds__(256) emit_kernel(const int32_t* __restrict__ v
     for (int tx = lo; tx <= hi; ++tx) {
       const int t = ty * rs.tiles_x + tx;
       const uint32_t o = __ldg(tile_start + t) + atomicAdd(cur + t, 1u);
-      if (o < cap) tile_vals[o] = static_cast<uint32_t>(i);
+      if (o < cap) tile_keys[o] = key;
     }
   }
 }
 
-// (key, source) total order of the reference's per-tile comparator (raster.cpp:78-83):
-// positive fp64 depths order as their bit patterns.
-__device__ __forceinline__ bool key_greater(uint64_t ka, uint32_t sa, uint64_t kb, uint32_t sb) {
-  return ka > kb || (ka == kb && sa > sb);
+__device__ __forceinline__ void cmpx(uint64_t& a, uint64_t& b) {  // a <- min, b <- max
+  const uint64_t lo = a < b ? a : b;
+  b = a < b ? b : a;
+  a = lo;
 }
 
-// Bitonic sort (flip formulation) of `len` entries, all compare-exchanges ascending and
-// entries at index >= len treated as +inf (never moved), over arrays K / S that are
-// shared or global memory. Called by all threads of the CTA.
-__device__ __forceinline__ void cmp_swap(uint64_t* keys, uint32_t* srcs, int lo, int hi) {
-  const uint64_t ka = keys[lo], kb = keys[hi];
-  const uint32_t sa = srcs[lo], sb = srcs[hi];
-  if (key_greater(ka, sa, kb, sb)) {
-    keys[lo] = kb; keys[hi] = ka;
-    srcs[lo] = sb; srcs[hi] = sa;
+// Bitonic sort of n = NT * E keys (flip formulation, all ascending), keys in
+// registers in blocked order (thread t holds t*E .. t*E+E-1). Partners closer than
+// E are in the same thread, closer than 32E in the same warp (shuffles), the rest go
+// through shared memory `sm` (n keys).
+template <int NT, int E, int M, bool FLIP>
+__device__ __forceinline__ void bitonic_step(uint64_t (&v)[E], uint64_t* sm, int t) {
+  if constexpr (M < E) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if ((e ^ M) > e) cmpx(v[e], v[e ^ M]);
+    }
+  } else if constexpr (M < 32 * E) {
+    constexpr int LM = M / E;  // lane distance (flip: k/E - 1, half-cleaner: j/E)
+    constexpr int TOP = FLIP ? ((LM + 1) >> 1) : LM;
+    const bool lower = (t & TOP) == 0;  // this lane holds the lower index of each pair
+    uint64_t w[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) w[e] = __shfl_xor_sync(0xffffffffu, v[FLIP ? (e ^ (E - 1)) : e], LM);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint64_t mn = v[e] < w[e] ? v[e] : w[e];
+      const uint64_t mx = v[e] < w[e] ? w[e] : v[e];
+      v[e] = lower ? mn : mx;
+    }
+  } else {
+    // striped layout: element (t, e) at sm[e * NT + t] (consecutive lanes, consecutive words)
+    constexpr int NTH = NT;
+    __syncthreads();  // previous readers of sm are done
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[e * NTH + t] = v[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = t * E + e, p = i ^ M;
+      const uint64_t w = sm[(p % E) * NTH + p / E];
+      const uint64_t mn = v[e] < w ? v[e] : w;
+      const uint64_t mx = v[e] < w ? w : v[e];
+      v[e] = i < p ? mn : mx;
+    }
   }
 }
 
-template <int NT>
-__device__ void bitonic_sort(uint64_t* keys, uint32_t* srcs, int len) {
-  int lg = 0;
-  while ((1 << lg) < len) ++lg;
-  const int half = 1 << (lg - 1);
-  for (int lk = 1; lk <= lg; ++lk) {
-    const int lh = lk - 1;  // log2(k / 2)
-    for (int i = threadIdx.x; i < half; i += NT) {  // flip
-      const int blk = i >> lh, off = i & ((1 << lh) - 1);
-      const int lo = (blk << lk) + off, hi = (blk << lk) + (1 << lk) - 1 - off;
-      if (hi < len) cmp_swap(keys, srcs, lo, hi);
+template <int NT, int E, int LK, int LJ>
+__device__ __forceinline__ void bitonic_stage(uint64_t (&v)[E], uint64_t* sm, int t) {
+  // stage k = 2^LK, step j = 2^LJ (LJ = LK - 1 is the flip step)
+  if constexpr (LJ == LK - 1) bitonic_step<NT, E, (1 << LK) - 1, true>(v, sm, t);
+  else bitonic_step<NT, E, (1 << LJ), false>(v, sm, t);
+  if constexpr (LJ > 0) bitonic_stage<NT, E, LK, LJ - 1>(v, sm, t);
+}
+
+template <int NT, int E, int LK, int LG>
+__device__ __forceinline__ void bitonic_all(uint64_t (&v)[E], uint64_t* sm, int t) {
+  bitonic_stage<NT, E, LK, LK - 1>(v, sm, t);
+  if constexpr (LK < LG) bitonic_all<NT, E, LK + 1, LG>(v, sm, t);
+}
+
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }
+
+// Bitonic sort of n = NT * E keys (flip formulation, all ascending), keys in
+// registers in blocked order (thread t holds t*E .. t*E+E-1). Partners closer than
+// E are in the same thread, closer than 32E in the same warp (shuffles), the rest go
+// through shared memory `sm` (n keys). Fully unrolled at compile time.
+template <int NT, int E>
+__device__ void bitonic_regs(uint64_t (&v)[E], uint64_t* sm) {
+  bitonic_all<NT, E, 1, ilog2(NT * E)>(v, sm, threadIdx.x);
+}
+
+// Sorts the bucket [start, start + len) of tile keys into tile_vals (sources). After
+// a truncated-key sort (sh > 0), runs of equal truncated depth are re-ordered by the
+// full (depth, source) order (rare).
+template <int NT, int E>
+__device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int start, int len,
+                            uint64_t* sm, const uint64_t* __restrict__ depth_bits, int sh, int src_bits) {
+  uint64_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = threadIdx.x * E + e;
+    v[e] = i < len ? keys[start + i] : ~0ull;
+  }
+  bitonic_regs<NT, E>(v, sm);
+  const uint64_t smask = (1ull << src_bits) - 1ull;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = threadIdx.x * E + e;
+    if (i < len) vals[start + i] = static_cast<uint32_t>(v[e] & smask);
+  }
+  if (sh > 0) {
+    __syncthreads();
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i + 1 < len; i += NT) {
+      const uint32_t a = vals[start + i], b = vals[start + i + 1];
+      const uint64_t da = depth_bits[a], db = depth_bits[b];
+      if (da > db || (da == db && a > b)) bad = 1;
     }
     __syncthreads();
-    for (int lj = lk - 2; lj >= 0; --lj) {  // half-cleaners, j = 2^lj
-      for (int i = threadIdx.x; i < half; i += NT) {
-        const int lo = ((i >> lj) << (lj + 1)) + (i & ((1 << lj) - 1)), hi = lo + (1 << lj);
-        if (hi < len) cmp_swap(keys, srcs, lo, hi);
+    if (bad && threadIdx.x == 0) {  // insertion sort by the full key (only ever on near-equal depths)
+      for (int i = 1; i < len; ++i) {
+        const uint32_t x = vals[start + i];
+        const uint64_t dx = depth_bits[x];
+        int j = i - 1;
+        while (j >= 0) {
+          const uint32_t y = vals[start + j];
+          const uint64_t dy = depth_bits[y];
+          if (!(dy > dx || (dy == dx && y > x))) break;
+          vals[start + j + 1] = y;
+          --j;
+        }
+        vals[start + j + 1] = x;
+      }
+    }
+  }
+}
+
+// NT = 256: buckets up to 4096 entries, sorted in n = 256 * E slots with E = 1, 2, 4,
+// 8 or 16 (the smallest power of two that fits); NT = 1024: 4097..16384 entries.
+template <int NT, bool LARGE>
+__global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restrict__ ranges,
+                                                        const uint64_t* __restrict__ keys,
+                                                        uint32_t* __restrict__ tile_vals,
+                                                        const uint64_t* __restrict__ depth_bits,
+                                                        const unsigned long long* __restrict__ depth_minmax,
+                                                        int src_bits) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* sm = reinterpret_cast<uint64_t*>(smem_raw);
+  const int t = blockIdx.x;
+  const int start = ranges[2 * t], len = ranges[2 * t + 1] - start;
+  const int sh = key_shift(depth_minmax, src_bits);
+  if (!LARGE) {
+    if (len <= 1 || len > 4096) return;
+    if (len <= 256) sort_bucket<NT, 1>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    else if (len <= 512) sort_bucket<NT, 2>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    else if (len <= 1024) sort_bucket<NT, 4>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    else if (len <= 2048) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    else sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+  } else {
+    if (len <= 4096 || len > 16384) return;
+    if (len <= 8192) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    else sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+  }
+}
+
+// Buckets beyond 16384 entries (never seen in the benchmark scenes): bitonic network
+// over global memory by one CTA, then sources written back.
+__global__ void __launch_bounds__(1024) sort_tiles_global_kernel(const int32_t* __restrict__ ranges,
+                                                                 uint64_t* __restrict__ keys,
+                                                                 uint32_t* __restrict__ tile_vals,
+                                                                 const uint64_t* __restrict__ depth_bits,
+                                                                 const unsigned long long* __restrict__ depth_minmax,
+                                                                 int src_bits) {
+  const int t = blockIdx.x;
+  const int start = ranges[2 * t], len = ranges[2 * t + 1] - start;
+  if (len <= 16384) return;
+  uint64_t* kk = keys + start;
+  int n = 1;
+  while (n < len) n <<= 1;
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int m = j == (k >> 1) ? k - 1 : j;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int p = i ^ m;
+        if (p > i && p < len) {
+          uint64_t a = kk[i], b = kk[p];
+          if (b < a) {
+            kk[i] = b;
+            kk[p] = a;
+          }
+        }
       }
       __syncthreads();
     }
   }
-}
-
-// One CTA per tile in the size class (lo_len, hi_len]; the smem class loads the bucket's
-// (depth bits, source) into shared memory, the last class sorts in global memory.
-template <int NT, int CAP, bool GLOBAL>
-__global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restrict__ ranges, int lo_len,
-                                                        const uint64_t* __restrict__ depth_bits,
-                                                        uint32_t* __restrict__ tile_vals, uint64_t* __restrict__ key_scratch) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int t = blockIdx.x;
-  const int start = ranges[2 * t], len = ranges[2 * t + 1] - start;
-  if (len <= lo_len || len <= 1 || (!GLOBAL && len > CAP)) return;
-  if (!GLOBAL) {
-    uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
-    uint32_t* srcs = reinterpret_cast<uint32_t*>(smem_raw + sizeof(uint64_t) * CAP);
-    for (int i = threadIdx.x; i < len; i += NT) {
-      const uint32_t s = tile_vals[start + i];
-      srcs[i] = s;
-      keys[i] = __ldg(depth_bits + s);
+  const uint64_t smask = (1ull << src_bits) - 1ull;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) tile_vals[start + i] = static_cast<uint32_t>(kk[i] & smask);
+  __syncthreads();
+  if (key_shift(depth_minmax, src_bits) > 0 && threadIdx.x == 0) {  // full-key fix-up (see sort_bucket)
+    for (int i = 1; i < len; ++i) {
+      const uint32_t x = tile_vals[start + i];
+      const uint64_t dx = depth_bits[x];
+      int j = i - 1;
+      while (j >= 0) {
+        const uint32_t y = tile_vals[start + j];
+        const uint64_t dy = depth_bits[y];
+        if (!(dy > dx || (dy == dx && y > x))) break;
+        tile_vals[start + j + 1] = y;
+        --j;
+      }
+      tile_vals[start + j + 1] = x;
     }
-    __syncthreads();
-    bitonic_sort<NT>(keys, srcs, len);
-    for (int i = threadIdx.x; i < len; i += NT) tile_vals[start + i] = srcs[i];
-  } else {
-    uint64_t* keys = key_scratch + start;
-    uint32_t* srcs = tile_vals + start;
-    for (int i = threadIdx.x; i < len; i += NT) keys[i] = __ldg(depth_bits + srcs[i]);
-    __syncthreads();
-    bitonic_sort<NT>(keys, srcs, len);
   }
 }
 
@@ -234,32 +384,35 @@ void launch_tile_scan(const uint32_t* tile_counts, int tiles, uint32_t cap, int3
 }
 
 void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const BinRec* bins, const DevRaster& rs,
-                 int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint32_t* tile_vals,
-                 cudaStream_t st) {
+                 int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint64_t* tile_keys,
+                 const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, cudaStream_t st) {
   if (n > 0)
-    emit_kernel<<<grid_for(n, 256), 256, 0, st>>>(valid, n, recs, bins, rs, img_h, cursor, tile_start, cap, tile_vals);
+    emit_kernel<<<grid_for(n, 256), 256, 0, st>>>(valid, n, recs, bins, rs, img_h, cursor, tile_start, cap, tile_keys,
+                                                  depth_bits, depth_minmax, src_bits);
 }
 
-template <int NT, int CAP, bool GLOBAL>
-void launch_sort_class(const int32_t* ranges, int tiles, int lo_len, const uint64_t* depth_bits, uint32_t* tile_vals,
-                       uint64_t* key_scratch, cudaStream_t st) {
-  constexpr int smem = GLOBAL ? 0 : static_cast<int>((sizeof(uint64_t) + sizeof(uint32_t)) * CAP);
+template <int NT, bool LARGE>
+void launch_sort_class(const int32_t* ranges, int tiles, const uint64_t* keys, uint32_t* tile_vals,
+                       const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
+                       cudaStream_t st) {
+  constexpr int smem = static_cast<int>(sizeof(uint64_t)) * (LARGE ? 16384 : 4096);
   static unsigned long long configured = 0;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!GLOBAL && !(configured >> dev & 1ull)) {
-    cudaFuncSetAttribute(sort_tiles_kernel<NT, CAP, GLOBAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (!(configured >> dev & 1ull)) {
+    cudaFuncSetAttribute(sort_tiles_kernel<NT, LARGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured |= 1ull << dev;
   }
-  sort_tiles_kernel<NT, CAP, GLOBAL><<<tiles, NT, smem, st>>>(ranges, lo_len, depth_bits, tile_vals, key_scratch);
+  sort_tiles_kernel<NT, LARGE><<<tiles, NT, smem, st>>>(ranges, keys, tile_vals, depth_bits, depth_minmax, src_bits);
 }
 
-void launch_sort_tiles(const int32_t* ranges, int tiles, const uint64_t* depth_bits, uint32_t* tile_vals,
-                       uint64_t* key_scratch, cudaStream_t st) {
+void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint32_t* tile_vals,
+                       const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
+                       cudaStream_t st) {
   if (tiles <= 0) return;
-  launch_sort_class<256, 4096, false>(ranges, tiles, 0, depth_bits, tile_vals, key_scratch, st);       // 48 KB
-  launch_sort_class<1024, 16384, false>(ranges, tiles, 4096, depth_bits, tile_vals, key_scratch, st);  // 192 KB
-  launch_sort_class<1024, 0, true>(ranges, tiles, 16384, depth_bits, tile_vals, key_scratch, st);      // global
+  launch_sort_class<256, false>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, st);
+  launch_sort_class<1024, true>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, st);
+  sort_tiles_global_kernel<<<tiles, 1024, 0, st>>>(ranges, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits);
 }
 
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n, uint64_t* keys_out,

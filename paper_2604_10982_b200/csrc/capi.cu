@@ -54,7 +54,7 @@ struct psm_ctx {
   psm_stage_times times{};
   psm_counters last{};
   // scratch
-  psm::Buf recs, bins, culls, depth_bits, tile_counts, cursor, tile_totals, tile_start, kscratch, valid, pos, keys_c, src_c, keys_s, src_s;
+  psm::Buf recs, bins, culls, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, valid, pos, keys_c, src_c, keys_s, src_s;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
@@ -207,7 +207,11 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->tile_start, tiles, &tstart));
     PSM_CUDA_TRY(cudaMemsetAsync(tcounts, 0, sizeof(uint32_t) * tiles * kSplit, st));
     // K1: projection, records, per-tile bucket sizes
-    launch_preprocess(sc->surfels, n, dc, rs, recs, bins, culls, dbits, tcounts, valid, n_proj_dev,
+    unsigned long long* dminmax;
+    PSM_TRY(ensure(ctx, ctx->dminmax, 2, &dminmax));
+    const unsigned long long init_minmax[2] = {~0ull, 0ull};
+    PSM_CUDA_TRY(cudaMemcpyAsync(dminmax, init_minmax, sizeof init_minmax, cudaMemcpyHostToDevice, st));
+    launch_preprocess(sc->surfels, n, dc, rs, recs, bins, culls, dbits, tcounts, valid, n_proj_dev, dminmax,
                       reinterpret_cast<int32_t*>(small), st);
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 1);
@@ -224,9 +228,11 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     key_cap = ctx->key_cap;
     if (key_cap > 0x7fffffffLL) return fail(ctx, PSM_EUNSUPPORTED, "RN-Total exceeds 2^31 tile assignments");
     uint32_t* tvals;
-    uint64_t* kscratch;
+    uint64_t* tkeys;
     PSM_TRY(ensure(ctx, ctx->tvals, key_cap, &tvals));
-    PSM_TRY(ensure(ctx, ctx->kscratch, key_cap, &kscratch));
+    PSM_TRY(ensure(ctx, ctx->kscratch, key_cap, &tkeys));
+    int src_bits = 1;
+    while ((int64_t{1} << src_bits) < n) ++src_bits;
 
     // K3: bucket offsets = per-tile ranges, RN-Total, non-empty tiles
     launch_tile_scan(tcounts, tiles, static_cast<uint32_t>(key_cap), ranges, cursor, ttotals, tstart, rn_dev,
@@ -234,11 +240,12 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 2);
     // K4: every (surfel, tile) pair into its tile's bucket
-    launch_emit(valid, n, recs, bins, rs, H, cursor, tstart, static_cast<uint32_t>(key_cap), tvals, st);
+    launch_emit(valid, n, recs, bins, rs, H, cursor, tstart, static_cast<uint32_t>(key_cap), tkeys, dbits, dminmax,
+                src_bits, st);
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 3);
     // K5: per-tile sort by (depth bits, source)
-    launch_sort_tiles(ranges, tiles, dbits, tvals, kscratch, st);
+    launch_sort_tiles(ranges, tiles, tkeys, tvals, dbits, dminmax, src_bits, st);
     PSM_CUDA_TRY(cudaGetLastError());
     tvals_s = tvals;
     record(ctx, 4);
@@ -506,7 +513,7 @@ int psm_destroy(psm_ctx* ctx) {
   if (!ctx) return PSM_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->culls, &ctx->depth_bits, &ctx->tile_counts, &ctx->cursor, &ctx->tile_totals, &ctx->tile_start, &ctx->kscratch, &ctx->valid, &ctx->pos,
+  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->culls, &ctx->depth_bits, &ctx->dminmax, &ctx->tile_counts, &ctx->cursor, &ctx->tile_totals, &ctx->tile_start, &ctx->kscratch, &ctx->valid, &ctx->pos,
                       &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s,
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
                       &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,

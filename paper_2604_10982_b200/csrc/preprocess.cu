@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const double* __restric
                                                           uint64_t* __restrict__ depth_bits,
                                                           uint32_t* __restrict__ tile_counts,
                                                           int32_t* __restrict__ valid, uint32_t* __restrict__ n_proj,
+                                                          unsigned long long* __restrict__ depth_minmax,
                                                           int32_t* __restrict__ err) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -188,9 +189,24 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const double* __restric
   depth_bits[i] = static_cast<uint64_t>(__double_as_longlong(zz));
   count_tiles(b, cx, cy, rs, cam.h, tile_counts);
   valid[i] = 1;
-  {  // n_proj: one atomic per warp
+  {  // n_proj and the frame's depth bit range (sort keys, binning.cu): one atomic each per warp
     const unsigned m = __activemask();
-    if ((threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(n_proj, static_cast<uint32_t>(__popc(m)));
+    const unsigned long long db = static_cast<unsigned long long>(__double_as_longlong(zz));
+    unsigned long long lo = db, hi = db;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long l2 = __shfl_xor_sync(m, lo, o), h2 = __shfl_xor_sync(m, hi, o);
+      const bool in = (m >> ((threadIdx.x & 31) ^ o)) & 1u;
+      if (in) {
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+      }
+    }
+    if ((threadIdx.x & 31) == __ffs(m) - 1) {
+      atomicAdd(n_proj, static_cast<uint32_t>(__popc(m)));
+      atomicMin(depth_minmax, lo);
+      atomicMax(depth_minmax + 1, hi);
+    }
   }
 }
 
@@ -198,11 +214,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const double* __restric
 
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
                        BinRec* bins, CullRec* culls, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,
-                       uint32_t* n_proj, int32_t* err, cudaStream_t stream) {
+                       uint32_t* n_proj, unsigned long long* depth_minmax, int32_t* err, cudaStream_t stream) {
   if (n <= 0) return;
   const int64_t blocks = (n + 255) / 256;
   preprocess_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(surfels13, n, cam, rs, recs, bins, culls, depth_bits,
-                                                                       tile_counts, valid, n_proj, err);
+                                                                       tile_counts, valid, n_proj, depth_minmax, err);
 }
 
 }  // namespace psm

@@ -32,17 +32,18 @@ struct BlendParams {
 // K1 preprocess.cu
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
                        BinRec* bins, CullRec* culls, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,
-                       uint32_t* n_proj, int32_t* err, cudaStream_t stream);
+                       uint32_t* n_proj, unsigned long long* depth_minmax, int32_t* err, cudaStream_t stream);
 
 // binning.cu
 void launch_tile_scan(const uint32_t* tile_counts, int tiles, uint32_t cap, int32_t* ranges, uint32_t* cursor,
                       uint32_t* totals, uint32_t* tile_start, uint32_t* rn_dev, uint32_t* rn_eff,
                       unsigned long long* nonempty, int32_t* overflow, cudaStream_t st);
 void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const BinRec* bins, const DevRaster& rs,
-                 int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint32_t* tile_vals,
-                 cudaStream_t st);
-void launch_sort_tiles(const int32_t* ranges, int tiles, const uint64_t* depth_bits, uint32_t* tile_vals,
-                       uint64_t* key_scratch, cudaStream_t st);
+                 int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint64_t* tile_keys,
+                 const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, cudaStream_t st);
+void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint32_t* tile_vals,
+                       const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
+                       cudaStream_t st);
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n,
                     uint64_t* keys_out, uint32_t* src_out, cudaStream_t st);
 void launch_rank_of(const uint32_t* src_by_rank, const uint32_t* n_proj_dev, int64_t cap, int32_t* rank_of,
