@@ -1,0 +1,349 @@
+// psimap_b200.hpp — C++ drop-in for the reference's render API, over the C-ABI (psm.h).
+//
+// Same namespace, names, argument meaning and error behaviour as the reference's
+// proj/include/psimap/raster.hpp:42-172 and core_types.hpp:17-111, without Eigen:
+//   psimap::render(scene, labels, cam, cfg)            raster.hpp:142-143
+//   psimap::render_into(out, scene, labels, cam, cfg)  raster.hpp:147-148
+//   psimap::bench_render(scene, labels, cam, reps, cfg) raster.hpp:171-172
+// Types keep the reference's field names (Surfel::center/rotation/scales/opacity/
+// color/f_sem/f_ins, Camera::r_cw/t_cw/fx/fy/cx/cy/width/height/near_clip/far_clip,
+// RasterConfig, RenderTargets with double Plane<> outputs in HWC layout). Small
+// fixed-size vectors replace Eigen's Vec2/3/4 and Mat3 (column-major like Eigen).
+// `labels` is the N_q x N column-major matrix the reference passes as `const MatX*`.
+//
+// Every render runs on the GPU (libpsm.so); there is no CPU fallback. A degenerate
+// quaternion throws std::invalid_argument like rotation_from_quat
+// (math_util.cpp:48-50); other failures throw std::runtime_error. RenderCache is
+// not supported (backward is out of scope): passing one throws.
+//
+// Link: -I<repo>/include -L<repo>/paper_2604_10982_b200 -lpsm
+#ifndef PSIMAP_B200_HPP
+#define PSIMAP_B200_HPP
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "psm.h"
+
+namespace psimap {
+
+template <int N>
+struct VecN {
+  std::array<double, N> v{};
+  double& operator[](int i) { return v[i]; }
+  double operator[](int i) const { return v[i]; }
+};
+using Vec2 = VecN<2>;
+using Vec3 = VecN<3>;
+using Vec4 = VecN<4>;
+inline Vec2 vec2(double a, double b) { return Vec2{{a, b}}; }
+inline Vec3 vec3(double a, double b, double c) { return Vec3{{a, b, c}}; }
+inline Vec4 vec4(double a, double b, double c, double d) { return Vec4{{a, b, c, d}}; }
+
+struct Mat3 {  // column-major like Eigen::Matrix3d
+  std::array<double, 9> m{{1, 0, 0, 0, 1, 0, 0, 0, 1}};
+  double& operator()(int r, int c) { return m[c * 3 + r]; }
+  double operator()(int r, int c) const { return m[c * 3 + r]; }
+  static Mat3 Identity() { return Mat3{}; }
+};
+
+struct VecX : std::vector<double> {  // Eigen::VectorXd stand-in
+  using std::vector<double>::vector;
+};
+
+// N_q x N, column-major: column s is surfel s's label distribution (const MatX*, raster.hpp:142)
+struct MatX {
+  int rows_ = 0, cols_ = 0;
+  std::vector<double> data_;
+  MatX() = default;
+  MatX(int r, int c, double fill = 0.0) : rows_(r), cols_(c), data_(static_cast<size_t>(r) * c, fill) {}
+  int rows() const { return rows_; }
+  int cols() const { return cols_; }
+  double& operator()(int r, int c) { return data_[static_cast<size_t>(c) * rows_ + r]; }
+  double operator()(int r, int c) const { return data_[static_cast<size_t>(c) * rows_ + r]; }
+  const double* data() const { return data_.data(); }
+};
+
+struct Surfel {  // core_types.hpp:17-25
+  Vec3 center{};
+  Vec4 rotation{{1, 0, 0, 0}};
+  Vec2 scales{{1, 1}};
+  double opacity = 0.5;
+  Vec3 color{};
+  VecX f_sem;
+  VecX f_ins;
+};
+
+struct Camera {  // core_types.hpp:36-53
+  Mat3 r_cw = Mat3::Identity();
+  Vec3 t_cw{};
+  double fx = 1, fy = 1, cx = 0, cy = 0;
+  int width = 0, height = 0;
+  double near_clip = 0.01, far_clip = 100.0;
+
+  static Camera from_c(const psm_camera& c) {
+    Camera o;
+    std::copy(c.r_cw, c.r_cw + 9, o.r_cw.m.begin());
+    for (int i = 0; i < 3; ++i) o.t_cw[i] = c.t_cw[i];
+    o.fx = c.fx; o.fy = c.fy; o.cx = c.cx; o.cy = c.cy;
+    o.width = c.width; o.height = c.height;
+    o.near_clip = c.near_clip; o.far_clip = c.far_clip;
+    return o;
+  }
+  psm_camera to_c() const {
+    psm_camera c{};
+    std::copy(r_cw.m.begin(), r_cw.m.end(), c.r_cw);
+    for (int i = 0; i < 3; ++i) c.t_cw[i] = t_cw[i];
+    c.fx = fx; c.fy = fy; c.cx = cx; c.cy = cy;
+    c.width = width; c.height = height;
+    c.near_clip = near_clip; c.far_clip = far_clip;
+    return c;
+  }
+  // Camera::make / look_at (core_types.cpp:18-60): throw std::invalid_argument on bad parameters
+  static Camera make(const Mat3& r, const Vec3& t, double fx, double fy, double cx, double cy, int w, int h,
+                     double near_clip, double far_clip) {
+    psm_camera c{};
+    if (psm_camera_make(r.m.data(), t.v.data(), fx, fy, cx, cy, w, h, near_clip, far_clip, &c) != PSM_OK)
+      throw std::invalid_argument("camera: invalid parameters");
+    return from_c(c);
+  }
+  static Camera look_at(const Vec3& eye, const Vec3& target, const Vec3& up, double fx, double fy, int w, int h,
+                        double near_clip, double far_clip) {
+    psm_camera c{};
+    if (psm_camera_look_at(eye.v.data(), target.v.data(), up.v.data(), fx, fy, w, h, near_clip, far_clip, &c) != PSM_OK)
+      throw std::invalid_argument("camera: invalid look_at");
+    return from_c(c);
+  }
+};
+
+struct SceneMap {  // core_types.hpp:102-111 (render-relevant part)
+  std::vector<Surfel> surfels;
+  std::vector<std::string> vocabulary;
+  int c_sem() const { return surfels.empty() ? 0 : static_cast<int>(surfels[0].f_sem.size()); }
+};
+
+template <typename T>
+struct Plane {  // image.hpp:11-43, HWC channel-fastest
+  int width = 0, height = 0, channels = 0;
+  std::vector<T> data;
+  Plane() = default;
+  Plane(int w, int h, int c, T fill = T{}) : width(w), height(h), channels(c), data(static_cast<size_t>(w) * h * c, fill) {}
+  T& at(int x, int y, int c = 0) { return data[(static_cast<size_t>(y) * width + x) * channels + c]; }
+  const T& at(int x, int y, int c = 0) const { return data[(static_cast<size_t>(y) * width + x) * channels + c]; }
+  T* pixel(int x, int y) { return &data[(static_cast<size_t>(y) * width + x) * channels]; }
+};
+using Image = Plane<double>;
+using IntPlane = Plane<int32_t>;
+
+enum class Binning { Circle = PSM_BIN_CIRCLE, Aabb = PSM_BIN_AABB, Ellipse = PSM_BIN_ELLIPSE };
+enum class Blending { Full = PSM_BLEND_FULL, TopK = PSM_BLEND_TOPK };
+
+struct RasterConfig {  // raster.hpp:42-54
+  int tile_size = 16;
+  double chi2 = 9.0;
+  double alpha_min = 1.0 / 255.0;
+  double t_min = 1e-4;
+  bool support_cutoff = true;
+  Binning binning = Binning::Aabb;
+  Blending blending = Blending::Full;
+  int top_k = 16;
+  Vec3 background{};
+  bool render_depth_normal = true;
+  int threads = 0;
+
+  psm_raster_config to_c() const {
+    psm_raster_config c{};
+    c.tile_size = tile_size; c.chi2 = chi2; c.alpha_min = alpha_min; c.t_min = t_min;
+    c.support_cutoff = support_cutoff; c.binning = static_cast<int>(binning);
+    c.blending = static_cast<int>(blending); c.top_k = top_k;
+    for (int i = 0; i < 3; ++i) c.background[i] = background[i];
+    c.render_depth_normal = render_depth_normal; c.threads = threads;
+    return c;
+  }
+};
+
+struct RenderTargets {  // raster.hpp:56-66
+  Image color, depth, normal, sem_feat, ins_dist;
+  IntPlane ins_argmax;
+  Image alpha_acc;
+  IntPlane blend_count;
+  uint64_t blended_total = 0;
+};
+
+struct RenderCache;  // backward-pass intermediates: out of scope on the GPU path
+
+struct BenchRow {  // raster.hpp:150-160
+  std::string name;
+  Binning binning;
+  Blending blending;
+  double time_ms = 0, fps = 0;
+  uint64_t rn_total = 0;
+  double rn_per_tile = 0;
+  uint64_t blended_total = 0;
+  double blended_per_pixel = 0;
+};
+struct BenchReport {  // raster.hpp:162-167
+  std::vector<BenchRow> rows;
+  int repetitions = 0, width = 0, height = 0, surfel_count = 0;
+};
+
+namespace b200 {
+
+// One context per device, created on first use (the reference keeps no globals; this
+// is plumbing: a CUDA stream and grow-only scratch reused across calls).
+inline psm_ctx* context(int device = 0) {
+  struct Holder {
+    psm_ctx* ctx = nullptr;
+    ~Holder() { if (ctx) psm_destroy(ctx); }
+  };
+  static thread_local Holder h;
+  if (!h.ctx) {
+    if (psm_create(device, nullptr, &h.ctx) != PSM_OK) throw std::runtime_error("psimap::b200: no CUDA device");
+  }
+  return h.ctx;
+}
+
+inline void check(int st, psm_ctx* ctx) {
+  if (st == PSM_OK) return;
+  const std::string msg = ctx ? psm_last_error(ctx) : "psm error";
+  if (st == PSM_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+// Flattens the scene and uploads it (the reference borrows the scene per call).
+struct UploadedScene {
+  psm_scene* sc = nullptr;
+  psm_ctx* ctx = nullptr;
+  ~UploadedScene() { if (sc) psm_scene_free(ctx, sc); }
+};
+
+inline std::unique_ptr<UploadedScene> upload(const SceneMap& scene, const MatX* labels, psm_ctx* ctx) {
+  const int64_t n = static_cast<int64_t>(scene.surfels.size());
+  const int c_sem = scene.c_sem();
+  std::vector<double> geo(static_cast<size_t>(n) * 13), fs(static_cast<size_t>(n) * c_sem);
+  for (int64_t i = 0; i < n; ++i) {
+    const Surfel& s = scene.surfels[i];
+    double* g = &geo[static_cast<size_t>(i) * 13];
+    for (int k = 0; k < 3; ++k) g[k] = s.center[k];
+    for (int k = 0; k < 4; ++k) g[3 + k] = s.rotation[k];
+    g[7] = s.scales[0]; g[8] = s.scales[1]; g[9] = s.opacity;
+    for (int k = 0; k < 3; ++k) g[10 + k] = s.color[k];
+    for (int c = 0; c < c_sem; ++c) fs[static_cast<size_t>(i) * c_sem + c] = s.f_sem[c];
+  }
+  auto u = std::make_unique<UploadedScene>();
+  u->ctx = ctx;
+  const int n_q = labels ? labels->rows() : 0;
+  check(psm_scene_upload(ctx, geo.data(), n, fs.data(), c_sem, labels ? labels->data() : nullptr, n_q, &u->sc), ctx);
+  return u;
+}
+
+template <typename T>
+inline void reset_plane(Plane<T>& p, int w, int h, int c) {  // raster.cpp:255-262
+  if (p.width != w || p.height != h || p.channels != c) p = Plane<T>(w, h, c);
+}
+
+}  // namespace b200
+
+// render_into (raster.cpp:273-511) on the GPU; outputs converted to the reference's double planes.
+inline void render_into(RenderTargets& out, const SceneMap& scene, const MatX* labels, const Camera& cam,
+                        const RasterConfig& cfg, RenderCache* cache = nullptr) {
+  if (cache) throw std::runtime_error("psimap::b200: RenderCache (backward) is not supported on the GPU path");
+  psm_ctx* ctx = b200::context();
+  auto up = b200::upload(scene, labels, ctx);
+  const int w = cam.width, h = cam.height, c_sem = scene.c_sem(), n_q = labels ? labels->rows() : 0;
+  const size_t npx = static_cast<size_t>(w) * h;
+  std::vector<float> col(npx * 3), dep(npx * 2), nrm(npx * 3), sem(npx * c_sem), ins(npx * n_q), alp(npx);
+  std::vector<int32_t> arg(npx), cnt(npx);
+  psm_targets tg{col.data(), dep.data(), nrm.data(), c_sem ? sem.data() : nullptr, n_q ? ins.data() : nullptr,
+                 arg.data(), alp.data(), cnt.data(), 0};
+  const psm_camera cc = cam.to_c();
+  const psm_raster_config rc = cfg.to_c();
+  psm_counters counters{};
+  b200::check(psm_render(ctx, up->sc, &cc, &rc, &tg, &counters), ctx);
+  b200::reset_plane(out.color, w, h, 3);
+  b200::reset_plane(out.depth, w, h, 2);
+  b200::reset_plane(out.normal, w, h, 3);
+  b200::reset_plane(out.sem_feat, w, h, c_sem);
+  b200::reset_plane(out.ins_dist, w, h, n_q);
+  b200::reset_plane(out.ins_argmax, w, h, 1);
+  b200::reset_plane(out.alpha_acc, w, h, 1);
+  b200::reset_plane(out.blend_count, w, h, 1);
+  std::copy(col.begin(), col.end(), out.color.data.begin());
+  std::copy(dep.begin(), dep.end(), out.depth.data.begin());
+  std::copy(nrm.begin(), nrm.end(), out.normal.data.begin());
+  std::copy(sem.begin(), sem.end(), out.sem_feat.data.begin());
+  std::copy(ins.begin(), ins.end(), out.ins_dist.data.begin());
+  std::copy(arg.begin(), arg.end(), out.ins_argmax.data.begin());
+  std::copy(alp.begin(), alp.end(), out.alpha_acc.data.begin());
+  std::copy(cnt.begin(), cnt.end(), out.blend_count.data.begin());
+  out.blended_total = counters.blended_total;
+}
+
+inline RenderTargets render(const SceneMap& scene, const MatX* labels, const Camera& cam, const RasterConfig& cfg,
+                            RenderCache* cache = nullptr) {
+  RenderTargets out;
+  render_into(out, scene, labels, cam, cfg, cache);
+  return out;
+}
+
+// bench_render (raster.cpp:513-573): the 4-row grid; the scene is uploaded once and
+// each row times `repetitions` whole renders (device clock, min), counters from the frame.
+inline BenchReport bench_render(const SceneMap& scene, const MatX* labels, const Camera& cam, int repetitions,
+                                const RasterConfig& base_cfg) {
+  psm_ctx* ctx = b200::context();
+  auto up = b200::upload(scene, labels, ctx);
+  BenchReport report;
+  report.repetitions = repetitions;
+  report.width = cam.width;
+  report.height = cam.height;
+  report.surfel_count = static_cast<int>(scene.surfels.size());
+  const std::array<std::pair<const char*, std::pair<Binning, Blending>>, 4> rows = {{
+      {"baseline", {Binning::Circle, Blending::Full}},
+      {"precise_tile", {Binning::Aabb, Blending::Full}},
+      {"topk", {Binning::Circle, Blending::TopK}},
+      {"full_method", {Binning::Aabb, Blending::TopK}},
+  }};
+  const psm_camera cc = cam.to_c();
+  psm_set_profiling(ctx, 1);
+  psm_targets tg{};  // planes stay in device scratch
+  tg.on_device = 1;
+  for (const auto& row : rows) {
+    RasterConfig cfg = base_cfg;
+    cfg.binning = row.second.first;
+    cfg.blending = row.second.second;
+    const psm_raster_config rc = cfg.to_c();
+    psm_counters counters{};
+    b200::check(psm_render(ctx, up->sc, &cc, &rc, &tg, &counters), ctx);  // warm-up
+    double best = 1e300;
+    for (int r = 0; r < std::max(repetitions, 1); ++r) {
+      b200::check(psm_render(ctx, up->sc, &cc, &rc, &tg, &counters), ctx);
+      psm_stage_times t{};
+      psm_get_stage_times(ctx, &t);
+      best = std::min(best, static_cast<double>(t.total));
+    }
+    BenchRow br;
+    br.name = row.first;
+    br.binning = cfg.binning;
+    br.blending = cfg.blending;
+    br.time_ms = best;
+    br.fps = best > 0 ? 1000.0 / best : 0;
+    br.rn_total = counters.rn_total;
+    br.rn_per_tile = counters.rn_per_tile;
+    br.blended_total = counters.blended_total;
+    br.blended_per_pixel = static_cast<double>(counters.blended_total) / (static_cast<double>(cam.width) * cam.height);
+    report.rows.push_back(br);
+  }
+  psm_set_profiling(ctx, 0);
+  return report;
+}
+
+}  // namespace psimap
+
+#endif  // PSIMAP_B200_HPP

@@ -408,12 +408,9 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
   PSM_TRY(pick(tg->blend_count, ctx->plane_cnt, npx, 4, reinterpret_cast<void**>(&pl.cnt)));
   pl.sem = nullptr;
   pl.ins = nullptr;
-  if (cs > 0 && (tg->sem_feat || !tg->on_device)) PSM_TRY(pick(tg->sem_feat, ctx->plane_sem, npx * cs, 4, reinterpret_cast<void**>(&pl.sem)));
-  if (nq > 0 && (tg->ins_dist || !tg->on_device)) PSM_TRY(pick(tg->ins_dist, ctx->plane_ins, npx * nq, 4, reinterpret_cast<void**>(&pl.ins)));
-  if (!tg->on_device) {
-    if (!tg->sem_feat) pl.sem = nullptr;
-    if (!tg->ins_dist) pl.ins = nullptr;
-  }
+  // feature planes are always produced (context scratch when the caller passes NULL)
+  if (cs > 0) PSM_TRY(pick(tg->sem_feat, ctx->plane_sem, npx * cs, 4, reinterpret_cast<void**>(&pl.sem)));
+  if (nq > 0) PSM_TRY(pick(tg->ins_dist, ctx->plane_ins, npx * nq, 4, reinterpret_cast<void**>(&pl.ins)));
   auto enqueue_d2h = [&]() -> int {
     if (tg->on_device) return PSM_OK;
     cudaStream_t st = ctx->stream;
@@ -427,8 +424,8 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
     PSM_TRY(d2h(tg->alpha_acc, pl.alpha, npx * 4));
     PSM_TRY(d2h(tg->ins_argmax, pl.arg, npx * 4));
     PSM_TRY(d2h(tg->blend_count, pl.cnt, npx * 4));
-    if (pl.sem) PSM_TRY(d2h(tg->sem_feat, pl.sem, npx * cs * 4));
-    if (pl.ins) PSM_TRY(d2h(tg->ins_dist, pl.ins, npx * nq * 4));
+    if (pl.sem && tg->sem_feat) PSM_TRY(d2h(tg->sem_feat, pl.sem, npx * cs * 4));
+    if (pl.ins && tg->ins_dist) PSM_TRY(d2h(tg->ins_dist, pl.ins, npx * nq * 4));
     return PSM_OK;
   };
   PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg));
