@@ -115,9 +115,9 @@ typedef struct psm_counters {
  *   tile_ranges [2 * tiles] [start, end) of each tile in tile_keys
  *   depth_order [cap_proj]  source index at each depth rank ((sort_depth, source)
  *               order of raster.cpp:78-83)
- *   topk_src    [W*H*K] selected source indices per pixel in blend order, -1 padded
- *               (topk_select, raster.cpp:225-251 + compaction 438-454); written
- *               when blending == TOPK. */
+ *   topk_src    [W*H*K] the set of selected source indices per pixel (ordered by
+ *               weight, -1 padded) (topk_select, raster.cpp:225-251 + compaction
+ *               438-454); written when blending == TOPK. */
 typedef struct psm_debug {
   uint64_t* tile_keys;
   int32_t* tile_vals;
