@@ -96,21 +96,31 @@ __device__ __forceinline__ void accumulate_row(float (&acc)[NV][VEC], float w, c
   }
 }
 
-// Can the (inflated) support ellipse of a candidate reach any pixel centre of the
-// warp's block [x0, x1] x [y0, y1] (already widened by the absolute margin)? The
-// ellipse's x-extent over the strip dy in [y0 - cy, y1 - cy] is its right edge
-// slope*dy + sqrt((kF11 - dy^2) dq) at the concave maximiser dstar clamped into the
-// strip (left edge: -dstar), as in psm_ellipse.h. fp32 with k inflated by 1e-4 and a
-// 0.02 px margin: conservative against the per-pixel fp64 test (raster.cpp:379).
-__device__ __forceinline__ bool cull_meets(const float4 a, const float4 b, float x0, float x1, float y0, float y1) {
-  const float cx = a.x, cy = a.y, ey = a.z, slope = a.w, dstar = b.x, kf11 = b.y, dq = b.z;
-  if (!(ey < __int_as_float(0x7f800000))) return true;  // ill-conditioned / non-finite: keep
+// Can the (inflated) support ellipse d^T Finv d <= chi2 of staged record r reach
+// any pixel centre of the warp's block [x0, x1] x [y0, y1] (already widened by the
+// absolute margin)? In F = Finv^-1 terms (Finv = [[a, b], [b, c]], D = ac - b^2):
+// half-height ey = sqrt(k a / D); over the strip dy in [y0 - cy, y1 - cy] the
+// ellipse's x-extent is slope*dy +- sqrt((k a / D - dy^2) D) / a with
+// slope = -b / a, the right edge maximised at dstar = -(b / D) sqrt(k D / c) clamped
+// into the strip (left edge at -dstar), as in psm_ellipse.h. fp32 with k inflated
+// by 1e-4 and a 0.02 px margin; ill-conditioned (D < 0.01 ac) or far-off-screen
+// footprints are always kept, so the per-pixel fp64 test (raster.cpp:379) never
+// passes where this says no.
+__device__ __forceinline__ bool cull_meets(const SurfRec& r, float k, float x0, float x1, float y0, float y1) {
+  const float a = static_cast<float>(r.f00), b = 0.5f * static_cast<float>(r.f01x2), c = static_cast<float>(r.f11);
+  const float cx = static_cast<float>(r.cx), cy = static_cast<float>(r.cy);
+  const float D = a * c - b * b;
+  if (!(D > 0.01f * a * c) || !(fabsf(cx) < 1e5f) || !(fabsf(cy) < 1e5f)) return true;
+  const float kf11 = k * a / D;
+  const float ey = sqrtf(kf11);
   const float dlo = fmaxf(y0 - cy, -ey), dhi = fminf(y1 - cy, ey);
   if (dlo > dhi) return false;
+  const float slope = -b / a;
+  const float dstar = -(b / D) * sqrtf(k * D / c);
   const float dr = fminf(fmaxf(dstar, dlo), dhi);
   const float dl = fminf(fmaxf(-dstar, dlo), dhi);
-  const float xr = cx + slope * dr + sqrtf(fmaxf(kf11 - dr * dr, 0.f) * dq);
-  const float xl = cx + slope * dl - sqrtf(fmaxf(kf11 - dl * dl, 0.f) * dq);
+  const float xr = cx + slope * dr + sqrtf(fmaxf(kf11 - dr * dr, 0.f) * D) / a;
+  const float xl = cx + slope * dl - sqrtf(fmaxf(kf11 - dl * dl, 0.f) * D) / a;
   return xl <= x1 && xr >= x0;
 }
 
@@ -159,13 +169,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   }
 
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
-  float4 cn0 = make_float4(0.f, 0.f, 0.f, 0.f), cn1 = cn0;  // next chunk's prefilter record (lane's candidate)
+  const float kcull = static_cast<float>(p.chi2) * 1.0001f;
   auto prefetch = [&](int base, int buf) {
     if (lane < kChunk && base + lane < end) {
       const int s = static_cast<int>(__ldg(p.vals + base + lane));
-      const float4* cr = reinterpret_cast<const float4*>(p.culls + s);
-      cn0 = __ldg(cr);
-      cn1 = __ldg(cr + 1);
       const char* g = reinterpret_cast<const char*>(p.recs + s);
       char* d = reinterpret_cast<char*>(&stage.rec[buf][lane]);
 #pragma unroll
@@ -179,7 +186,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   for (int base = start; base < end; base += kChunk, buf ^= 1) {
     if (__all_sync(0xffffffffu, done)) break;
     const int cnt = min(kChunk, end - base);
-    const float4 c0 = cn0, c1 = cn1;
     if (base + kChunk < end) {
       prefetch(base + kChunk, buf ^ 1);
       cp_async_wait<1>();
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
     const SurfRec* recs = stage.rec[buf];
     // candidates that reach no pixel centre of this warp's block are skipped as a whole
     unsigned live = (1u << cnt) - 1u;  // cnt <= 30
-    if (p.support_cutoff) live = __ballot_sync(0xffffffffu, lane < cnt && cull_meets(c0, c1, bx0, bx1, by0, by1));
+    if (p.support_cutoff) live = __ballot_sync(0xffffffffu, lane < cnt && cull_meets(recs[lane], kcull, bx0, bx1, by0, by1));
     if (!done) {
       while (live) {
         const int j = __ffs(live) - 1;

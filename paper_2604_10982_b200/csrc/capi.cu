@@ -54,7 +54,7 @@ struct psm_ctx {
   psm_stage_times times{};
   psm_counters last{};
   // scratch
-  psm::Buf recs, bins, culls, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, valid, pos, keys_c, src_c, keys_s, src_s;
+  psm::Buf recs, bins, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, valid, pos, keys_c, src_c, keys_s, src_s;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
@@ -194,11 +194,10 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   uint32_t* tvals_s = nullptr;
   int64_t key_cap = 0;
   if (n > 0) {
-    SurfRec* recs; BinRec* bins; CullRec* culls; uint64_t* dbits; int32_t* valid;
+    SurfRec* recs; BinRec* bins; uint64_t* dbits; int32_t* valid;
     uint32_t *tcounts, *cursor, *ttotals, *tstart;
     PSM_TRY(ensure(ctx, ctx->recs, n, &recs));
     PSM_TRY(ensure(ctx, ctx->bins, n, &bins));
-    PSM_TRY(ensure(ctx, ctx->culls, n, &culls));
     PSM_TRY(ensure(ctx, ctx->depth_bits, n, &dbits));
     PSM_TRY(ensure(ctx, ctx->valid, n, &valid));
     PSM_TRY(ensure(ctx, ctx->tile_counts, static_cast<size_t>(tiles) * kSplit, &tcounts));
@@ -211,7 +210,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->dminmax, 2, &dminmax));
     const unsigned long long init_minmax[2] = {~0ull, 0ull};
     PSM_CUDA_TRY(cudaMemcpyAsync(dminmax, init_minmax, sizeof init_minmax, cudaMemcpyHostToDevice, st));
-    launch_preprocess(sc->surfels, n, dc, rs, recs, bins, culls, dbits, tcounts, valid, n_proj_dev, dminmax,
+    launch_preprocess(sc->surfels, n, dc, rs, recs, bins, dbits, tcounts, valid, n_proj_dev, dminmax,
                       reinterpret_cast<int32_t*>(small), st);
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 1);
@@ -256,7 +255,6 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   bp.ranges = ranges;
   bp.vals = tvals_s;
   bp.recs = static_cast<const SurfRec*>(ctx->recs.p);
-  bp.culls = static_cast<const CullRec*>(ctx->culls.p);
   bp.feat = sc->feat;
   bp.feat_dims = feat_dims; bp.c_sem = sc->c_sem; bp.n_q = sc->n_q;
   bp.width = W; bp.height = H; bp.tiles_x = tiles_x;
@@ -510,7 +508,7 @@ int psm_destroy(psm_ctx* ctx) {
   if (!ctx) return PSM_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->culls, &ctx->depth_bits, &ctx->dminmax, &ctx->tile_counts, &ctx->cursor, &ctx->tile_totals, &ctx->tile_start, &ctx->kscratch, &ctx->valid, &ctx->pos,
+  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->depth_bits, &ctx->dminmax, &ctx->tile_counts, &ctx->cursor, &ctx->tile_totals, &ctx->tile_start, &ctx->kscratch, &ctx->valid, &ctx->pos,
                       &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s,
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
                       &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,

@@ -36,7 +36,7 @@ __device__ __forceinline__ void count_tiles(const BinRec& b, double cx, double c
 
 __global__ void __launch_bounds__(256) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
                                                           DevCamera cam, DevRaster rs, SurfRec* __restrict__ recs,
-                                                          BinRec* __restrict__ bins, CullRec* __restrict__ culls,
+                                                          BinRec* __restrict__ bins,
                                                           uint64_t* __restrict__ depth_bits,
                                                           uint32_t* __restrict__ tile_counts,
                                                           int32_t* __restrict__ valid, uint32_t* __restrict__ n_proj,
@@ -167,25 +167,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const double* __restric
   b.ty1 = min(x86_cvt(floor(y1 / ts)), rs.tiles_y - 1);
   b.pad0 = b.pad1 = 0;
   bins[i] = b;
-  {  // fp32 prefilter constants (conservative: k inflated by 1e-4; ill-conditioned -> never skip)
-    const double kk = rs.chi2 * 1.0001;
-    const double tr = F00 + F11;
-    CullRec c;
-    c.cx = static_cast<float>(cx);
-    c.cy = static_cast<float>(cy);
-    if (fdet > 0.0 && tr * tr < 1e10 * fdet && fabs(cx) < 1e7 && fabs(cy) < 1e7) {
-      c.ey = static_cast<float>(sqrt(kk * F11));
-      c.slope = static_cast<float>(F01 / F11);
-      c.dstar = static_cast<float>(F01 * sqrt(kk / F00));
-      c.kf11 = static_cast<float>(kk * F11);
-      c.dq = static_cast<float>(fdet / (F11 * F11));
-    } else {
-      c.ey = __int_as_float(0x7f800000);  // +inf: always a candidate
-      c.slope = c.dstar = c.kf11 = c.dq = 0.f;
-    }
-    c.pad = 0.f;
-    culls[i] = c;
-  }
   depth_bits[i] = static_cast<uint64_t>(__double_as_longlong(zz));
   count_tiles(b, cx, cy, rs, cam.h, tile_counts);
   valid[i] = 1;
@@ -213,11 +194,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const double* __restric
 }  // namespace
 
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
-                       BinRec* bins, CullRec* culls, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,
+                       BinRec* bins, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,
                        uint32_t* n_proj, unsigned long long* depth_minmax, int32_t* err, cudaStream_t stream) {
   if (n <= 0) return;
   const int64_t blocks = (n + 255) / 256;
-  preprocess_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(surfels13, n, cam, rs, recs, bins, culls, depth_bits,
+  preprocess_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(surfels13, n, cam, rs, recs, bins, depth_bits,
                                                                        tile_counts, valid, n_proj, depth_minmax, err);
 }
 

@@ -36,21 +36,6 @@ struct __align__(16) BinRec {
 };
 static_assert(sizeof(BinRec) == 48, "BinRec must be 48 bytes");
 
-// fp32 prefilter record [N] 32 B: constants of the support ellipse's x-extent over a
-// horizontal strip (the formulation of psm_ellipse.h, with k = chi2 (1 + 1e-4)),
-// used by the blend kernel to skip candidates that reach no pixel of a warp's
-// 8x4 block. ey = +inf marks an ill-conditioned footprint (never skipped).
-struct __align__(16) CullRec {
-  float cx, cy;  // screen centre
-  float ey;      // sqrt(k F11): half-height of the ellipse
-  float slope;   // F01 / F11: centre line x = slope * dy
-  float dstar;   // F01 sqrt(k / F00): dy of the rightmost point
-  float kf11;    // k F11
-  float dq;      // det F / F11^2: half-width(dy) = sqrt((k F11 - dy^2) dq)
-  float pad;
-};
-static_assert(sizeof(CullRec) == 32, "CullRec must be 32 bytes");
-
 // Sub-buckets per tile for the counting sort's atomics (binning.cu).
 constexpr int kSplit = 32;
 

@@ -13,7 +13,6 @@ struct BlendParams {
   const int32_t* ranges;  // [tiles][2]
   const uint32_t* vals;   // tile-sorted source ids
   const SurfRec* recs;
-  const CullRec* culls;
   const float* feat;      // [N][feat_dims]: f_sem | labels, fp32
   int32_t feat_dims, c_sem, n_q;
   int32_t width, height, tiles_x;
@@ -31,7 +30,7 @@ struct BlendParams {
 
 // K1 preprocess.cu
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
-                       BinRec* bins, CullRec* culls, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,
+                       BinRec* bins, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,
                        uint32_t* n_proj, unsigned long long* depth_minmax, int32_t* err, cudaStream_t stream);
 
 // binning.cu
