@@ -290,13 +290,11 @@ Grid bin(const std::vector<Projected>& projected, const Cam& cam, int ts, double
     tx1 = std::min(tx1, g.tiles_x - 1);
     ty1 = std::min(ty1, g.tiles_y - 1);
     const M2 f = footprint_cov(p.sigma);
+    PsmEllipse e{};
+    if (binning == 2) e = psm_ellipse_prep(p.center[0], p.center[1], f.at(0, 0), f.at(0, 1), f.at(1, 1), chi2);
     for (int ty = ty0; ty <= ty1; ++ty) {
       int lo = tx0, hi = tx1;
-      if (binning == 2 &&
-          !psm_ellipse_row(p.center[0], p.center[1], f.at(0, 0), f.at(0, 1), f.at(1, 1), chi2, ty, ts,
-                           cam.h, tx0, tx1, &lo, &hi)) {
-        continue;
-      }
+      if (binning == 2 && !psm_ellipse_row(e, ty, ts, cam.h, tx0, tx1, &lo, &hi)) continue;
       for (int tx = lo; tx <= hi; ++tx) g.tiles[static_cast<size_t>(ty) * g.tiles_x + tx].push_back(static_cast<int>(i));
     }
   }

@@ -135,18 +135,35 @@ __global__ void __launch_bounds__(256) emit_kernel(const int32_t* __restrict__ v
   const BinRec b = bins[i];
   if (b.tx0 > b.tx1 || b.ty0 > b.ty1) return;
   const bool ellipse = rs.binning == PSM_BIN_ELLIPSE;
-  const double cx = recs[i].cx, cy = recs[i].cy;
+  PsmEllipse e;
+  if (ellipse) e = psm_ellipse_prep(recs[i].cx, recs[i].cy, b.F00, b.F01, b.F11, rs.chi2);
   uint32_t* cur = cursor + static_cast<int64_t>(threadIdx.x & (kSplit - 1)) * rs.tiles_x * rs.tiles_y;
+  // tiles are claimed in batches of kBatch so several returning atomics are in flight at once
+  constexpr int kBatch = 8;
+  int pend[kBatch];
+  int np = 0;
+  auto flush = [&]() {
+    uint32_t o[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (u < np) o[u] = atomicAdd(cur + pend[u], 1u);
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (u < np) {
+        const uint32_t at = __ldg(tile_start + pend[u]) + o[u];
+        if (at < cap) tile_keys[at] = key;
+      }
+    np = 0;
+  };
   for (int ty = b.ty0; ty <= b.ty1; ++ty) {
     int lo = b.tx0, hi = b.tx1;
-    if (ellipse && !psm_ellipse_row(cx, cy, b.F00, b.F01, b.F11, rs.chi2, ty, rs.tile_size, img_h, b.tx0, b.tx1, &lo, &hi))
-      continue;
+    if (ellipse && !psm_ellipse_row(e, ty, rs.tile_size, img_h, b.tx0, b.tx1, &lo, &hi)) continue;
     for (int tx = lo; tx <= hi; ++tx) {
-      const int t = ty * rs.tiles_x + tx;
-      const uint32_t o = __ldg(tile_start + t) + atomicAdd(cur + t, 1u);
-      if (o < cap) tile_keys[o] = key;
+      pend[np++] = ty * rs.tiles_x + tx;
+      if (np == kBatch) flush();
     }
   }
+  if (np) flush();
 }
 
 __device__ __forceinline__ void cmpx(uint64_t& a, uint64_t& b) {  // a <- min, b <- max

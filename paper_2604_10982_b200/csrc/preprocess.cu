@@ -23,18 +23,19 @@ __device__ __forceinline__ double sum3(double a, double b, double c) { return (a
 __device__ __forceinline__ void count_tiles(const BinRec& b, double cx, double cy, const DevRaster& rs, int img_h,
                                             uint32_t* __restrict__ tile_counts) {
   if (b.tx0 > b.tx1 || b.ty0 > b.ty1) return;
+  const bool ellipse = rs.binning == PSM_BIN_ELLIPSE;
+  PsmEllipse e;
+  if (ellipse) e = psm_ellipse_prep(cx, cy, b.F00, b.F01, b.F11, rs.chi2);
   for (int ty = b.ty0; ty <= b.ty1; ++ty) {
     int lo = b.tx0, hi = b.tx1;
-    if (rs.binning == PSM_BIN_ELLIPSE &&
-        !psm_ellipse_row(cx, cy, b.F00, b.F01, b.F11, rs.chi2, ty, rs.tile_size, img_h, b.tx0, b.tx1, &lo, &hi))
-      continue;
+    if (ellipse && !psm_ellipse_row(e, ty, rs.tile_size, img_h, b.tx0, b.tx1, &lo, &hi)) continue;
     uint32_t* row = tile_counts + static_cast<int64_t>(threadIdx.x & (kSplit - 1)) * rs.tiles_x * rs.tiles_y +
                     ty * rs.tiles_x;
     for (int tx = lo; tx <= hi; ++tx) atomicAdd(row + tx, 1u);
   }
 }
 
-__global__ void __launch_bounds__(256) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
+__global__ void __launch_bounds__(256, 3) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
                                                           DevCamera cam, DevRaster rs, SurfRec* __restrict__ recs,
                                                           BinRec* __restrict__ bins,
                                                           uint64_t* __restrict__ depth_bits,

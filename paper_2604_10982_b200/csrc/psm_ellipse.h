@@ -28,16 +28,38 @@
 #include <math.h>
 #endif
 
-// Tile-column run [*tx_lo, *tx_hi] of tile row `ty` met by the ellipse of a
-// surfel centred at (cx, cy) with dilated covariance (f00, f01, f11). The run
-// is intersected with the AABB columns [ax0, ax1]. Returns 0 if the row is empty.
-PSM_EHD int psm_ellipse_row(double cx, double cy, double f00, double f01, double f11, double chi2,
-                            int ty, int ts, int height, int ax0, int ax1, int* tx_lo,
-                            int* tx_hi) {
+// Per-surfel constants of the row test (computed once per surfel, used per tile row).
+struct PsmEllipse {
+  double cx, cy;
+  double ymax;   // sqrt(k F11): y half-extent
+  double slope;  // F01 / F11: centre line x = slope * dy
+  double dstar;  // F01 sqrt(k / F00): dy of the rightmost point
+  double kf11;   // k F11
+  double q;      // det F / F11^2: half-width(dy) = sqrt((k F11 - dy^2) q)
+  int ok;        // 0: degenerate / ill-conditioned -> every AABB row is kept
+};
+
+PSM_EHD PsmEllipse psm_ellipse_prep(double cx, double cy, double f00, double f01, double f11, double chi2) {
+  PsmEllipse e;
   const double k = chi2 * 1.000001 + 1e-9;
   const double det = f00 * f11 - f01 * f01;
   const double tr = f00 + f11;
-  if (!(det > 0.0) || !(tr * tr < 1e12 * det)) {  // degenerate / ill-conditioned: keep AABB row
+  e.cx = cx;
+  e.cy = cy;
+  e.ok = (det > 0.0) && (tr * tr < 1e12 * det);
+  e.ymax = e.ok ? sqrt(k * f11) : 0.0;
+  e.slope = e.ok ? f01 / f11 : 0.0;
+  e.dstar = e.ok ? f01 * sqrt(k / f00) : 0.0;
+  e.kf11 = k * f11;
+  e.q = e.ok ? det / (f11 * f11) : 0.0;
+  return e;
+}
+
+// Tile-column run [*tx_lo, *tx_hi] of tile row `ty` met by the ellipse, intersected
+// with the AABB columns [ax0, ax1]. Returns 0 if the row is empty.
+PSM_EHD int psm_ellipse_row(const PsmEllipse& e, int ty, int ts, int height, int ax0, int ax1, int* tx_lo,
+                            int* tx_hi) {
+  if (!e.ok) {  // degenerate / ill-conditioned: keep the AABB row
     *tx_lo = ax0;
     *tx_hi = ax1;
     return ax0 <= ax1;
@@ -46,26 +68,23 @@ PSM_EHD int psm_ellipse_row(double cx, double cy, double f00, double f01, double
   int y_end = ty * ts + ts;
   if (y_end > height) y_end = height;
   const double y_hi = y_end - 0.5;
-  const double ymax = sqrt(k * f11);
-  double dlo = y_lo - cy;
-  double dhi = y_hi - cy;
-  if (dlo < -ymax) dlo = -ymax;
-  if (dhi > ymax) dhi = ymax;
+  double dlo = y_lo - e.cy;
+  double dhi = y_hi - e.cy;
+  if (dlo < -e.ymax) dlo = -e.ymax;
+  if (dhi > e.ymax) dhi = e.ymax;
   if (dlo > dhi + 1e-3) return 0;  // strip misses the ellipse's y-extent
-  const double slope = f01 / f11;
-  const double dstar = f01 * sqrt(k / f00);
-  double dr = dstar;               // maximiser of the right edge, clamped into the strip
+  double dr = e.dstar;             // maximiser of the right edge, clamped into the strip
   if (dr < dlo) dr = dlo;
   if (dr > dhi) dr = dhi;
-  double dl = -dstar;              // minimiser of the left edge
+  double dl = -e.dstar;            // minimiser of the left edge
   if (dl < dlo) dl = dlo;
   if (dl > dhi) dl = dhi;
-  double rr = k * f11 - dr * dr;
-  double rl = k * f11 - dl * dl;
+  double rr = e.kf11 - dr * dr;
+  double rl = e.kf11 - dl * dl;
   if (rr < 0.0) rr = 0.0;
   if (rl < 0.0) rl = 0.0;
-  const double xr = cx + slope * dr + sqrt(rr * det) / f11 + 1e-3;
-  const double xl = cx + slope * dl - sqrt(rl * det) / f11 - 1e-3;
+  const double xr = e.cx + e.slope * dr + sqrt(rr * e.q) + 1e-3;
+  const double xl = e.cx + e.slope * dl - sqrt(rl * e.q) - 1e-3;
   // tiles whose pixel-centre span [tx*ts + 0.5, tx*ts + ts - 0.5] meets [xl, xr]
   double lo = ceil((xl - (ts - 0.5)) / ts);
   double hi = floor((xr - 0.5) / ts);
