@@ -11,10 +11,10 @@
 //                  (atomic cursor; order inside a bucket is arbitrary)
 //   K5 sort_tiles  one CTA per tile sorts its bucket by the total order
 //                  (fp64 depth bits, source), packed into one 64-bit key, with a
-//                  bitonic network held in registers (shuffles within a warp,
-//                  shared memory beyond), so the result is the reference's list
-//                  whatever order K4 produced. Size classes: <= 4096 entries
-//                  (256 threads), <= 16384 (1024 threads), larger over global memory.
+//                  block merge sort (register-sorted runs, merge-path rounds in
+//                  shared memory), so the result is the reference's list whatever
+//                  order K4 produced. Size classes: <= 4096 entries (128 threads),
+//                  <= 16384 (1024 threads), larger by a bitonic network over global memory.
 // Every count stays on the device; key buffers are capacity-checked (the host
 // re-renders a frame whose RN-Total outgrew them, capi.cu).
 #include "psm_device.cuh"
@@ -239,6 +239,52 @@ __device__ void bitonic_regs(uint64_t (&v)[E], uint64_t* sm) {
   bitonic_all<NT, E, 1, ilog2(NT * E)>(v, sm, threadIdx.x);
 }
 
+// Block merge sort of n = NT * E keys (ascending; keys are unique, padding ~0):
+// each thread sorts its E keys in registers, then log2(NT) rounds merge pairs of
+// sorted runs through shared memory `sm` (n keys); in each round a thread finds its
+// first output by a merge-path binary search and emits E outputs sequentially.
+// Shared-memory slot of logical key i: XOR-swizzled within 16-key groups so the
+// blocked stores (thread t writes keys tE .. tE+E-1) do not pile onto one bank.
+__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
+
+template <int NT, int E>
+__device__ void merge_sort_regs(uint64_t (&v)[E], uint64_t* sm) {
+  constexpr int n = NT * E;
+  bitonic_all<1, E, 1, ilog2(E)>(v, sm, 0);  // E keys in registers (register steps only)
+  const int t = threadIdx.x;
+#pragma unroll 1
+  for (int width = E; width < n; width <<= 1) {
+    __syncthreads();  // previous round's readers are done
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm[swz(t * E + e)] = v[e];
+    __syncthreads();
+    const int out0 = t * E;
+    const int base = out0 & ~(2 * width - 1);
+    const int a0 = base, b0 = base + width;
+    const int diag = out0 - base;
+    int lo = diag > width ? diag - width : 0, hi = diag < width ? diag : width;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sm[swz(a0 + mid)] < sm[swz(b0 + diag - 1 - mid)]) lo = mid + 1;
+      else hi = mid;
+    }
+    int ia = lo, ib = diag - lo;
+    uint64_t ka = ia < width ? sm[swz(a0 + ia)] : ~0ull, kb = ib < width ? sm[swz(b0 + ib)] : ~0ull;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const bool take_a = ka <= kb && ia < width;
+      v[e] = take_a ? ka : kb;
+      if (take_a) {
+        ++ia;
+        ka = ia < width ? sm[swz(a0 + ia)] : ~0ull;
+      } else {
+        ++ib;
+        kb = ib < width ? sm[swz(b0 + ib)] : ~0ull;
+      }
+    }
+  }
+}
+
 // Sorts the bucket [start, start + len) of tile keys into tile_vals (sources). After
 // a truncated-key sort (sh > 0), runs of equal truncated depth are re-ordered by the
 // full (depth, source) order (rare).
@@ -251,23 +297,25 @@ __device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restr
     const int i = threadIdx.x * E + e;
     v[e] = i < len ? keys[start + i] : ~0ull;
   }
-  bitonic_regs<NT, E>(v, sm);
+  merge_sort_regs<NT, E>(v, sm);
   const uint64_t smask = (1ull << src_bits) - 1ull;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = threadIdx.x * E + e;
-    if (i < len) vals[start + i] = static_cast<uint32_t>(v[e] & smask);
+    if (i < len) {
+      vals[start + i] = static_cast<uint32_t>(v[e] & smask);
+      // neighbours with equal truncated depth: order unknown below the dropped bits
+      if (sh > 0 && e + 1 < E && i + 1 < len && (v[e] >> src_bits) == (v[e + 1] >> src_bits)) bad = 1;
+    }
   }
   if (sh > 0) {
+    const int last = threadIdx.x * E + E - 1;  // pairs across thread boundaries
+    sm[threadIdx.x] = v[0];
     __syncthreads();
-    __shared__ int bad;
-    if (threadIdx.x == 0) bad = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i + 1 < len; i += NT) {
-      const uint32_t a = vals[start + i], b = vals[start + i + 1];
-      const uint64_t da = depth_bits[a], db = depth_bits[b];
-      if (da > db || (da == db && a > b)) bad = 1;
-    }
+    if (threadIdx.x + 1 < NT && last + 1 < len && (v[E - 1] >> src_bits) == (sm[threadIdx.x + 1] >> src_bits)) bad = 1;
     __syncthreads();
     if (bad && threadIdx.x == 0) {  // insertion sort by the full key (only ever on near-equal depths)
       for (int i = 1; i < len; ++i) {
@@ -287,8 +335,8 @@ __device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restr
   }
 }
 
-// NT = 256: buckets up to 4096 entries, sorted in n = 256 * E slots with E = 1, 2, 4,
-// 8 or 16 (the smallest power of two that fits); NT = 1024: 4097..16384 entries.
+// NT = 128: buckets up to 2048 entries in n = 128 * E slots (E = 2 .. 16, the smallest
+// that fits), 2049..4096 with E = 32; NT = 1024 (LARGE): 4097..16384 entries.
 template <int NT, bool LARGE>
 __global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restrict__ ranges,
                                                         const uint64_t* __restrict__ keys,
@@ -303,11 +351,11 @@ __global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restric
   const int sh = key_shift(depth_minmax, src_bits);
   if (!LARGE) {
     if (len <= 1 || len > 4096) return;
-    if (len <= 256) sort_bucket<NT, 1>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-    else if (len <= 512) sort_bucket<NT, 2>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-    else if (len <= 1024) sort_bucket<NT, 4>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-    else if (len <= 2048) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-    else sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    if (len <= 256) sort_bucket<NT, 2>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    else if (len <= 512) sort_bucket<NT, 4>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    else if (len <= 1024) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    else if (len <= 2048) sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    else sort_bucket<NT, 32>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
   } else {
     if (len <= 4096 || len > 16384) return;
     if (len <= 8192) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
@@ -427,7 +475,7 @@ void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, ui
                        const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
                        cudaStream_t st) {
   if (tiles <= 0) return;
-  launch_sort_class<256, false>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, st);
+  launch_sort_class<128, false>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, st);
   launch_sort_class<1024, true>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, st);
   sort_tiles_global_kernel<<<tiles, 1024, 0, st>>>(ranges, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits);
 }

@@ -35,16 +35,15 @@ __device__ __forceinline__ void count_tiles(const BinRec& b, double cx, double c
   }
 }
 
-__global__ void __launch_bounds__(256, 3) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
+// One surfel; returns whether it projects (then *db = its depth bit pattern).
+__device__ __forceinline__ bool project_one(int64_t i, const double* __restrict__ surfels13,
                                                           DevCamera cam, DevRaster rs, SurfRec* __restrict__ recs,
                                                           BinRec* __restrict__ bins,
                                                           uint64_t* __restrict__ depth_bits,
                                                           uint32_t* __restrict__ tile_counts,
-                                                          int32_t* __restrict__ valid, uint32_t* __restrict__ n_proj,
-                                                          unsigned long long* __restrict__ depth_minmax,
+                                                          int32_t* __restrict__ valid, 
+                                                          uint64_t* db,
                                                           int32_t* __restrict__ err) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
   const double* s = surfels13 + 13 * i;
   valid[i] = 0;
 
@@ -53,14 +52,14 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const double* __rest
   const double pc0 = sum3(cam.r[0] * mu0, cam.r[3] * mu1, cam.r[6] * mu2) + cam.t[0];
   const double pc1 = sum3(cam.r[1] * mu0, cam.r[4] * mu1, cam.r[7] * mu2) + cam.t[1];
   const double pc2 = sum3(cam.r[2] * mu0, cam.r[5] * mu1, cam.r[8] * mu2) + cam.t[2];
-  if (!(pc2 > cam.near_clip) || !(pc2 < cam.far_clip)) return;  // raster.cpp:97
+  if (!(pc2 > cam.near_clip) || !(pc2 < cam.far_clip)) return false;  // raster.cpp:97
 
   // rotation_from_quat (math_util.cpp:46-52): norm as Eigen's SSE2 Vector4d reduction
   const double qw = s[3], qx = s[4], qy = s[5], qz = s[6];
   const double qn = sqrt((qw * qw + qy * qy) + (qx * qx + qz * qz));
   if (!(qn > 1e-12) || !isfinite(qw) || !isfinite(qx) || !isfinite(qy) || !isfinite(qz)) {
     atomicOr(err, 1);  // the reference throws std::invalid_argument here
-    return;
+    return false;
   }
   const double w = qw / qn, x = qx / qn, y = qy / qn, z = qz / qn;
   // rotation_unit (math_util.cpp:16-23), R(row, col)
@@ -89,7 +88,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const double* __rest
   const double nb = sqrt(sum3(b0 * b0, b1 * b1, b2 * b2));
   const double np = sqrt(sum3(pc0 * pc0, pc1 * pc1, pc2 * pc2));
   const double det_scale = na * nb * np;
-  if (fabs(det) <= 1e-12 * (det_scale < 1e-30 ? 1e-30 : det_scale)) return;  // grazing, std::max (raster.cpp:109)
+  if (fabs(det) <= 1e-12 * (det_scale < 1e-30 ? 1e-30 : det_scale)) return false;  // grazing, std::max (raster.cpp:109)
 
   // Matrix3d::inverse: cofactors (cyclic), det from column 0, times 1/det
   const double c00 = m11 * m22 - m12 * m21;  // cof(0,0)
@@ -130,7 +129,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const double* __rest
   const double disc = sqrt(dd < 0.0 ? 0.0 : dd);  // std::max(., 0.0) keeps NaN
   const double rad = sqrt(rs.chi2 * (half_tr + disc));
   const double bx0 = cx - rad, bx1 = cx + rad, by0 = cy - rad, by1 = cy + rad;
-  if (bx1 < 0 || bx0 > cam.w || by1 < 0 || by0 > cam.h) return;
+  if (bx1 < 0 || bx0 > cam.w || by1 < 0 || by0 > cam.h) return false;
 
   // footprint_inv = adj(F) / det F (raster.cpp:132-136)
   rec.cx = cx;
@@ -171,24 +170,35 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const double* __rest
   depth_bits[i] = static_cast<uint64_t>(__double_as_longlong(zz));
   count_tiles(b, cx, cy, rs, cam.h, tile_counts);
   valid[i] = 1;
-  {  // n_proj and the frame's depth bit range (sort keys, binning.cu): one atomic each per warp
-    const unsigned m = __activemask();
-    const unsigned long long db = static_cast<unsigned long long>(__double_as_longlong(zz));
-    unsigned long long lo = db, hi = db;
+  *db = static_cast<uint64_t>(__double_as_longlong(zz));
+  return true;
+}
+
+__global__ void __launch_bounds__(256, 3) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
+                                                          DevCamera cam, DevRaster rs, SurfRec* __restrict__ recs,
+                                                          BinRec* __restrict__ bins,
+                                                          uint64_t* __restrict__ depth_bits,
+                                                          uint32_t* __restrict__ tile_counts,
+                                                          int32_t* __restrict__ valid, uint32_t* __restrict__ n_proj,
+                                                          unsigned long long* __restrict__ depth_minmax,
+                                                          int32_t* __restrict__ err) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t db = 0;
+  const bool ok = i < n && project_one(i, surfels13, cam, rs, recs, bins, depth_bits, tile_counts, valid, &db, err);
+  // n_proj and the frame's depth bit range (sort keys, binning.cu): a full-warp reduction
+  // with identities for culled lanes, one atomic each per warp
+  unsigned long long lo = ok ? db : ~0ull, hi = ok ? db : 0ull;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long l2 = __shfl_xor_sync(m, lo, o), h2 = __shfl_xor_sync(m, hi, o);
-      const bool in = (m >> ((threadIdx.x & 31) ^ o)) & 1u;
-      if (in) {
-        lo = l2 < lo ? l2 : lo;
-        hi = h2 > hi ? h2 : hi;
-      }
-    }
-    if ((threadIdx.x & 31) == __ffs(m) - 1) {
-      atomicAdd(n_proj, static_cast<uint32_t>(__popc(m)));
-      atomicMin(depth_minmax, lo);
-      atomicMax(depth_minmax + 1, hi);
-    }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = h2 > hi ? h2 : hi;
+  }
+  const unsigned ballot = __ballot_sync(0xffffffffu, ok);
+  if ((threadIdx.x & 31) == 0 && ballot) {
+    atomicAdd(n_proj, static_cast<uint32_t>(__popc(ballot)));
+    atomicMin(depth_minmax, lo);
+    atomicMax(depth_minmax + 1, hi);
   }
 }
 
