@@ -473,11 +473,17 @@ void launch_sort_class(const int32_t* ranges, int tiles, const uint64_t* keys, u
 
 void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint32_t* tile_vals,
                        const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
-                       cudaStream_t st) {
+                       cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
   if (tiles <= 0) return;
+  // The few large buckets (one 1024-thread CTA per SM) run on a side stream, concurrently
+  // with the many small ones, which fit beside them on every SM.
+  cudaEventRecord(fork, st);
+  cudaStreamWaitEvent(side, fork, 0);
+  launch_sort_class<1024, true>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, side);
+  sort_tiles_global_kernel<<<tiles, 1024, 0, side>>>(ranges, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits);
   launch_sort_class<128, false>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, st);
-  launch_sort_class<1024, true>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, st);
-  sort_tiles_global_kernel<<<tiles, 1024, 0, st>>>(ranges, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits);
+  cudaEventRecord(join, side);
+  cudaStreamWaitEvent(st, join, 0);
 }
 
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n, uint64_t* keys_out,

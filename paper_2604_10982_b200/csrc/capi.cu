@@ -47,6 +47,8 @@ struct psm_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t side = nullptr;   // concurrent side work within a frame (large tile buckets)
+  cudaEvent_t fork = nullptr, join = nullptr;
   std::string err;
   bool profiling = false;
   cudaEvent_t ev[8] = {};
@@ -244,7 +246,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 3);
     // K5: per-tile sort by (depth bits, source)
-    launch_sort_tiles(ranges, tiles, tkeys, tvals, dbits, dminmax, src_bits, st);
+    launch_sort_tiles(ranges, tiles, tkeys, tvals, dbits, dminmax, src_bits, st, ctx->side, ctx->fork, ctx->join);
     PSM_CUDA_TRY(cudaGetLastError());
     tvals_s = tvals;
     record(ctx, 4);
@@ -498,6 +500,12 @@ int psm_create(int device, void* stream, psm_ctx** out) {
     ctx->own_stream = true;
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming) != cudaSuccess) {
+    delete ctx;
+    return PSM_ECUDA;
+  }
   if (cudaMallocHost(&ctx->h_small, 8 * sizeof(int64_t)) != cudaSuccess) { delete ctx; return PSM_ENOMEM; }
   std::memset(ctx->h_small, 0, 8 * sizeof(int64_t));
   *out = ctx;
@@ -516,6 +524,9 @@ int psm_destroy(psm_ctx* ctx) {
                       &ctx->plane_arg, &ctx->plane_alpha, &ctx->plane_cnt};
   for (psm::Buf* b : bufs) psm::free_buf(*b);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+  if (ctx->fork) cudaEventDestroy(ctx->fork);
+  if (ctx->join) cudaEventDestroy(ctx->join);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

@@ -42,7 +42,7 @@ void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const Bin
                  const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, cudaStream_t st);
 void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint32_t* tile_vals,
                        const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
-                       cudaStream_t st);
+                       cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n,
                     uint64_t* keys_out, uint32_t* src_out, cudaStream_t st);
 void launch_rank_of(const uint32_t* src_by_rank, const uint32_t* n_proj_dev, int64_t cap, int32_t* rank_of,
