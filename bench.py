@@ -27,7 +27,10 @@ WORKLOADS = {
     "c2": (1_000_000, 1280, 720, 0, "full", 16, "1M surfels 1280x720 RGB+depth+normal"),
     "c3": (1_000_000, 1280, 720, 64, "topk", 8, "1M surfels 1280x720 64-d semantics Top-K=8"),
     "c4": (5_000_000, 1920, 1080, 128, "topk", 16, "5M surfels 1920x1080 128-d semantics Top-K=16"),
+    "c5": (5_000_000, 1920, 1080, 128, "topk", 16, "256-view trajectory over 5M surfels 1920x1080 128-d Top-K=16, "
+                                                     "views sharded across ranks"),
 }
+C5_VIEWS = 256
 METRIC = "panoptic frames/s at 1M surfels, 1280x720, 64-d feats, K=8; % HBM roofline"
 
 
@@ -102,10 +105,16 @@ def build_workload(name, rank, world):
     t0 = time.perf_counter()
     scene, _, cam0 = make_street_scene(StreetSpec(n_surfels=n, image_w=w, image_h=h, c_sem=c,
                                                   scale_mult=density_scale(n, w, h)), with_labels=False)
-    # weak scaling: rank r renders trajectory view r (view 0 == the street camera)
-    cam = cam0 if rank == 0 else trajectory_cameras(1, w, h, first=rank, count=1)[0]
+    if name == "c5":
+        # the rank's contiguous block of the closed-form 256-view trajectory
+        from paper_2604_10982_b200.multiview import shard_range
+        views = list(shard_range(C5_VIEWS, world, rank))
+        cams = trajectory_cameras(C5_VIEWS, w, h, first=views[0], count=len(views)) if views else []
+    else:
+        # weak scaling: rank r renders trajectory view r (view 0 == the street camera)
+        cams = [cam0 if rank == 0 else trajectory_cameras(1, w, h, first=rank, count=1)[0]]
     log(f"[rank {rank}] workload {name}: {len(scene)} surfels generated in {time.perf_counter() - t0:.1f}s")
-    return scene, cam, (n, w, h, c, blending, k, desc)
+    return scene, cams, (n, w, h, c, blending, k, desc)
 
 
 def raster_cfg(blending, k, reference=False):
@@ -133,7 +142,8 @@ def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
         return 0
-    scene, cam, (n, w, h, c, blending, k, desc) = build_workload(args.workload, 0, 1)
+    scene, cams, (n, w, h, c, blending, k, desc) = build_workload(args.workload, 0, 1)
+    cam = cams[0]
     cfg = raster_cfg(blending, k, reference=True)
     for _ in range(args.warmup):
         cpu_reference(scene, cam, cfg, 1)
@@ -167,7 +177,8 @@ def run_ours(args):
     from paper_2604_10982_b200 import Renderer
     from paper_2604_10982_b200 import _abi as A
 
-    scene, cam, (n, w, h, c, blending, k, desc) = build_workload(args.workload, rank, world)
+    scene, cams, (n, w, h, c, blending, k, desc) = build_workload(args.workload, rank, world)
+    cam = cams[0]
     cfg = raster_cfg(blending, k)
     stream = torch.cuda.Stream(device=dev)
     r = Renderer(local_rank, stream=stream.cuda_stream)
@@ -206,13 +217,20 @@ def run_ours(args):
             with torch.cuda.stream(stream):
                 flush.zero_()
                 ev[i][0].record(stream)
-            r.render_device(ds, cam, cfg, ptrs, counters=False)
+            for cv in cams:
+                r.render_device(ds, cv, cfg, ptrs, counters=False)
+                if len(cams) > 1:
+                    r.sync()
+                    st = r.stage_times()
+                    blend_ms.append(st["blend"])
+                    stage.append(st)
             with torch.cuda.stream(stream):
                 ev[i][1].record(stream)
-            r.sync()
-            st = r.stage_times()
-            blend_ms.append(st["blend"])
-            stage.append(st)
+            if len(cams) == 1:
+                r.sync()
+                st = r.stage_times()
+                blend_ms.append(st["blend"])
+                stage.append(st)
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
@@ -258,7 +276,8 @@ def run_ours(args):
             torch.distributed.destroy_process_group()
         return 0
 
-    frames = args.steps * world
+    views_total = C5_VIEWS if args.workload == "c5" else world
+    frames = args.steps * views_total
     value = frames / (total_ms / 1000.0)
     b_frame, b_blend = alg_bytes(n, n_proj, w, h, c)
     peaks = {}
@@ -295,7 +314,8 @@ def run_ours(args):
                    "blending": blending, "top_k": k, "surfels": n, "n_proj": n_proj, "width": w, "height": h,
                    "c_sem": c, "rn_total": int(cnt.rn_total), "blended_total": int(cnt.blended_total),
                    "l2": "flushed between timed steps (256 MB write outside the events)",
-                   "views_per_rank_per_step": 1, "parallelism": f"view-sharded x{world}, scene replicated",
+                   "views_per_rank_per_step": len(cams),
+                   "parallelism": f"view-sharded x{world}, scene replicated",
                    "stage_ms": stage_avg, "alg_bytes_per_frame": b_frame},
         "roofline": {"bound": "hbm", "kernel": "blend_kernel (K7)", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -313,6 +333,31 @@ def run_ours(args):
     return 0
 
 
+def run_grid(args):
+    """The reference's bench_render ablation grid (raster.cpp:513-573, Table 3 rows) on the GPU, plus
+    the Ellipse (exact precise-tile) rows: one JSON line with every row (min of `steps` device times)."""
+    import torch
+    from paper_2604_10982_b200 import Binning, Renderer, bench_render
+    torch.cuda.set_device(0)
+    scene, cams, (n, w, h, c, blending, k, desc) = build_workload(args.workload, 0, 1)
+    r = Renderer(0, stream=torch.cuda.current_stream().cuda_stream)
+    ds = r.upload(scene)
+    out = {"grid": args.workload, "desc": desc, "top_k": k, "rows": []}
+    for precise in (Binning.Aabb, Binning.Ellipse):
+        rep = bench_render(ds, None, cams[0], max(args.steps, 1), raster_cfg(blending, k), renderer=r,
+                           binnings=precise)
+        for row in rep.rows:
+            if precise == Binning.Ellipse and row.binning == Binning.Circle:
+                continue
+            out["rows"].append({"name": row.name if precise == Binning.Aabb else row.name + "_ellipse",
+                                "binning": row.binning.name, "blending": row.blending.name,
+                                "time_ms": row.time_ms, "fps": row.fps, "rn_total": row.rn_total,
+                                "rn_per_tile": row.rn_per_tile, "blended_total": row.blended_total,
+                                "blended_per_pixel": row.blended_per_pixel})
+    print(json.dumps(out), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -321,7 +366,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--grid", action="store_true", help="print the bench_render ablation grid instead")
     args = ap.parse_args()
+    if args.grid:
+        return run_grid(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -363,54 +363,104 @@ __global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restric
   }
 }
 
-// Buckets beyond 16384 entries (never seen in the benchmark scenes): bitonic network
-// over global memory by one CTA, then sources written back.
-__global__ void __launch_bounds__(1024) sort_tiles_global_kernel(const int32_t* __restrict__ ranges,
-                                                                 uint64_t* __restrict__ keys,
-                                                                 uint32_t* __restrict__ tile_vals,
-                                                                 const uint64_t* __restrict__ depth_bits,
-                                                                 const unsigned long long* __restrict__ depth_minmax,
-                                                                 int src_bits) {
-  const int t = blockIdx.x;
-  const int start = ranges[2 * t], len = ranges[2 * t + 1] - start;
-  if (len <= 16384) return;
-  uint64_t* kk = keys + start;
-  int n = 1;
-  while (n < len) n <<= 1;
-  for (int k = 2; k <= n; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const int m = j == (k >> 1) ? k - 1 : j;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int p = i ^ m;
-        if (p > i && p < len) {
-          uint64_t a = kk[i], b = kk[p];
-          if (b < a) {
-            kk[i] = b;
-            kk[p] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  const uint64_t smask = (1ull << src_bits) - 1ull;
-  for (int i = threadIdx.x; i < len; i += blockDim.x) tile_vals[start + i] = static_cast<uint32_t>(kk[i] & smask);
+// Full-key fix-up after a truncated-key sort (see sort_bucket): checks adjacent
+// entries of a sorted bucket and, if any pair is out of (depth, source) order,
+// insertion-sorts the bucket by the full key (thread 0; only on near-equal depths).
+__device__ void fixup_full_order(uint32_t* __restrict__ vals, int len, const uint64_t* __restrict__ depth_bits) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
   __syncthreads();
-  if (key_shift(depth_minmax, src_bits) > 0 && threadIdx.x == 0) {  // full-key fix-up (see sort_bucket)
+  for (int i = threadIdx.x; i + 1 < len; i += blockDim.x) {
+    const uint32_t a = vals[i], b = vals[i + 1];
+    const uint64_t da = depth_bits[a], db = depth_bits[b];
+    if (da > db || (da == db && a > b)) bad = 1;
+  }
+  __syncthreads();
+  if (bad && threadIdx.x == 0) {
     for (int i = 1; i < len; ++i) {
-      const uint32_t x = tile_vals[start + i];
+      const uint32_t x = vals[i];
       const uint64_t dx = depth_bits[x];
       int j = i - 1;
       while (j >= 0) {
-        const uint32_t y = tile_vals[start + j];
+        const uint32_t y = vals[j];
         const uint64_t dy = depth_bits[y];
         if (!(dy > dx || (dy == dx && y > x))) break;
-        tile_vals[start + j + 1] = y;
+        vals[j + 1] = y;
         --j;
       }
-      tile_vals[start + j + 1] = x;
+      vals[j + 1] = x;
     }
   }
+}
+
+// Buckets beyond 16384 entries (C4's largest is ~17.7k): one 1024-thread CTA sorts each
+// 16384-key chunk in shared memory, then merge-path passes in global memory double the
+// sorted run width until the bucket is one run (ping-pong with `scratch`).
+constexpr int kHugeChunk = 16384;
+__global__ void __launch_bounds__(1024) sort_tiles_huge_kernel(const int32_t* __restrict__ ranges,
+                                                               uint64_t* __restrict__ keys,
+                                                               uint64_t* __restrict__ scratch,
+                                                               uint32_t* __restrict__ tile_vals,
+                                                               const uint64_t* __restrict__ depth_bits,
+                                                               const unsigned long long* __restrict__ depth_minmax,
+                                                               int src_bits) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* sm = reinterpret_cast<uint64_t*>(smem_raw);
+  const int t = blockIdx.x;
+  const int start = ranges[2 * t], len = ranges[2 * t + 1] - start;
+  if (len <= kHugeChunk) return;
+  constexpr int NT = 1024, E = kHugeChunk / NT;
+  uint64_t* src = keys + start;
+  uint64_t* dst = scratch + start;
+  for (int c0 = 0; c0 < len; c0 += kHugeChunk) {  // sorted runs of kHugeChunk
+    const int cl = min(kHugeChunk, len - c0);
+    uint64_t v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = threadIdx.x * E + e;
+      v[e] = i < cl ? src[c0 + i] : ~0ull;
+    }
+    merge_sort_regs<NT, E>(v, sm);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = threadIdx.x * E + e;
+      if (i < cl) src[c0 + i] = v[e];
+    }
+    __syncthreads();
+  }
+  const int per = (len + NT - 1) / NT;  // outputs per thread in each merge pass
+  for (int width = kHugeChunk; width < len; width <<= 1) {
+    int o = threadIdx.x * per;
+    const int o_end = min(len, o + per);
+    while (o < o_end) {
+      const int base = (o / (2 * width)) * (2 * width);
+      const int na = min(width, len - base);
+      const int nb = min(width, max(0, len - base - width));
+      const uint64_t* A = src + base;
+      const uint64_t* B = src + base + width;
+      const int diag = o - base;
+      int lo = diag > nb ? diag - nb : 0, hi = diag < na ? diag : na;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (A[mid] < B[diag - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+      }
+      int ia = lo, ib = diag - lo;
+      const int seg_end = min(o_end, base + 2 * width);
+      for (; o < seg_end; ++o) {
+        const bool take_a = ib >= nb || (ia < na && A[ia] < B[ib]);
+        dst[o] = take_a ? A[ia++] : B[ib++];
+      }
+    }
+    __syncthreads();
+    uint64_t* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+  const uint64_t smask = (1ull << src_bits) - 1ull;
+  for (int i = threadIdx.x; i < len; i += NT) tile_vals[start + i] = static_cast<uint32_t>(src[i] & smask);
+  __syncthreads();
+  if (key_shift(depth_minmax, src_bits) > 0) fixup_full_order(tile_vals + start, len, depth_bits);
 }
 
 __global__ void compact_kernel(const int32_t* __restrict__ valid, const int32_t* __restrict__ pos,
@@ -471,7 +521,7 @@ void launch_sort_class(const int32_t* ranges, int tiles, const uint64_t* keys, u
   sort_tiles_kernel<NT, LARGE><<<tiles, NT, smem, st>>>(ranges, keys, tile_vals, depth_bits, depth_minmax, src_bits);
 }
 
-void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint32_t* tile_vals,
+void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint64_t* key_scratch, uint32_t* tile_vals,
                        const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
                        cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
   if (tiles <= 0) return;
@@ -480,7 +530,18 @@ void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, ui
   cudaEventRecord(fork, st);
   cudaStreamWaitEvent(side, fork, 0);
   launch_sort_class<1024, true>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, side);
-  sort_tiles_global_kernel<<<tiles, 1024, 0, side>>>(ranges, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits);
+  {
+    constexpr int smem = static_cast<int>(sizeof(uint64_t)) * kHugeChunk;
+    static unsigned long long configured = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(configured >> dev & 1ull)) {
+      cudaFuncSetAttribute(sort_tiles_huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      configured |= 1ull << dev;
+    }
+    sort_tiles_huge_kernel<<<tiles, 1024, smem, side>>>(ranges, tile_keys, key_scratch, tile_vals, depth_bits,
+                                                        depth_minmax, src_bits);
+  }
   launch_sort_class<128, false>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, st);
   cudaEventRecord(join, side);
   cudaStreamWaitEvent(st, join, 0);

@@ -56,7 +56,7 @@ struct psm_ctx {
   psm_stage_times times{};
   psm_counters last{};
   // scratch
-  psm::Buf recs, bins, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, valid, pos, keys_c, src_c, keys_s, src_s;
+  psm::Buf recs, bins, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, kscratch2, valid, pos, keys_c, src_c, keys_s, src_s;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
@@ -229,9 +229,10 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     key_cap = ctx->key_cap;
     if (key_cap > 0x7fffffffLL) return fail(ctx, PSM_EUNSUPPORTED, "RN-Total exceeds 2^31 tile assignments");
     uint32_t* tvals;
-    uint64_t* tkeys;
+    uint64_t *tkeys, *tkeys2;
     PSM_TRY(ensure(ctx, ctx->tvals, key_cap, &tvals));
     PSM_TRY(ensure(ctx, ctx->kscratch, key_cap, &tkeys));
+    PSM_TRY(ensure(ctx, ctx->kscratch2, key_cap, &tkeys2));
     int src_bits = 1;
     while ((int64_t{1} << src_bits) < n) ++src_bits;
 
@@ -246,7 +247,8 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 3);
     // K5: per-tile sort by (depth bits, source)
-    launch_sort_tiles(ranges, tiles, tkeys, tvals, dbits, dminmax, src_bits, st, ctx->side, ctx->fork, ctx->join);
+    launch_sort_tiles(ranges, tiles, tkeys, tkeys2, tvals, dbits, dminmax, src_bits, st, ctx->side, ctx->fork,
+                      ctx->join);
     PSM_CUDA_TRY(cudaGetLastError());
     tvals_s = tvals;
     record(ctx, 4);
@@ -516,7 +518,7 @@ int psm_destroy(psm_ctx* ctx) {
   if (!ctx) return PSM_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->depth_bits, &ctx->dminmax, &ctx->tile_counts, &ctx->cursor, &ctx->tile_totals, &ctx->tile_start, &ctx->kscratch, &ctx->valid, &ctx->pos,
+  psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->depth_bits, &ctx->dminmax, &ctx->tile_counts, &ctx->cursor, &ctx->tile_totals, &ctx->tile_start, &ctx->kscratch, &ctx->kscratch2, &ctx->valid, &ctx->pos,
                       &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s,
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
                       &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,

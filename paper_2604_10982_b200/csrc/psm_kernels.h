@@ -40,7 +40,7 @@ void launch_tile_scan(const uint32_t* tile_counts, int tiles, uint32_t cap, int3
 void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const BinRec* bins, const DevRaster& rs,
                  int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint64_t* tile_keys,
                  const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, cudaStream_t st);
-void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint32_t* tile_vals,
+void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint64_t* key_scratch, uint32_t* tile_vals,
                        const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
                        cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n,

@@ -221,3 +221,25 @@ def test_gpu_c3_binning_output_identity(rend, c3):
     bc = outs[0].blend_count
     assert outs[0].blended_total == int(np.minimum(bc, 8).sum())
     assert np.all(outs[0].alpha_acc >= 0) and np.all(outs[0].alpha_acc <= 1)
+
+
+@pytest.mark.parametrize("count", [5000, 20000])
+def test_gpu_huge_buckets_and_depth_ties(rend, count):
+    """Buckets beyond the 4096 and 16384 shared-memory sort classes (the merge-path global passes), with
+    exact depth ties broken by source index (raster.cpp:78-83)."""
+    rng = np.random.default_rng(count)
+    cam = front_camera(48, 48, 60.0)
+    z = rng.choice(np.linspace(2.0, 6.0, count // 4), size=count)  # every depth shared by ~4 surfels
+    xy = rng.uniform(-0.02, 0.02, size=(count, 2)) * z[:, None]
+    rows = np.zeros((count, 13))
+    rows[:, 0:2] = xy
+    rows[:, 2] = z
+    rows[:, 3] = 1.0
+    rows[:, 7] = rng.uniform(0.005, 0.02, count) * z
+    rows[:, 8] = rng.uniform(0.005, 0.02, count) * z
+    rows[:, 9] = rng.uniform(0.02, 0.1, count)
+    rows[:, 10:13] = rng.uniform(0, 1, (count, 3))
+    sc = SceneMap(rows, rng.standard_normal((count, 8)))
+    g, o = assert_parity(rend, sc, None, cam, RasterConfig(binning=Binning.Aabb, blending=Blending.TopK, top_k=8))
+    tiles = O.bin_surfels(rows, cam, RasterConfig(), 1)["tiles"]
+    assert max(len(t) for t in tiles) > (16384 if count > 16384 else 4096)
