@@ -285,12 +285,41 @@ __device__ void merge_sort_regs(uint64_t (&v)[E], uint64_t* sm) {
   }
 }
 
+// Repair after a truncated-key sort (sh > 0): entries whose truncated depths are equal
+// were ordered by source, not by (full depth, source). Each maximal run of equal
+// truncated depth is insertion-sorted by the full key by the thread owning its first
+// entry, all runs in parallel. Repairing a run only permutes entries of equal truncated
+// depth, so concurrent readers of a run's border always see the same truncated key.
+__device__ void repair_truncated_runs(uint32_t* __restrict__ vals, int len, const uint64_t* __restrict__ depth_bits,
+                                      uint64_t dmin, int sh) {
+  for (int i = threadIdx.x; i + 1 < len; i += blockDim.x) {
+    const uint64_t ti = (depth_bits[vals[i]] - dmin) >> sh;
+    if (i > 0 && ((depth_bits[vals[i - 1]] - dmin) >> sh) == ti) continue;  // not a run start
+    int j = i + 1;
+    while (j < len && ((depth_bits[vals[j]] - dmin) >> sh) == ti) ++j;
+    for (int a = i + 1; a < j; ++a) {
+      const uint32_t x = vals[a];
+      const uint64_t dx = depth_bits[x];
+      int b = a - 1;
+      while (b >= i) {
+        const uint32_t y = vals[b];
+        const uint64_t dy = depth_bits[y];
+        if (!(dy > dx || (dy == dx && y > x))) break;
+        vals[b + 1] = y;
+        --b;
+      }
+      vals[b + 1] = x;
+    }
+  }
+}
+
 // Sorts the bucket [start, start + len) of tile keys into tile_vals (sources). After
 // a truncated-key sort (sh > 0), runs of equal truncated depth are re-ordered by the
 // full (depth, source) order (rare).
 template <int NT, int E>
 __device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int start, int len,
-                            uint64_t* sm, const uint64_t* __restrict__ depth_bits, int sh, int src_bits) {
+                            uint64_t* sm, const uint64_t* __restrict__ depth_bits, uint64_t dmin, int sh,
+                            int src_bits) {
   uint64_t v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -317,21 +346,7 @@ __device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restr
     __syncthreads();
     if (threadIdx.x + 1 < NT && last + 1 < len && (v[E - 1] >> src_bits) == (sm[threadIdx.x + 1] >> src_bits)) bad = 1;
     __syncthreads();
-    if (bad && threadIdx.x == 0) {  // insertion sort by the full key (only ever on near-equal depths)
-      for (int i = 1; i < len; ++i) {
-        const uint32_t x = vals[start + i];
-        const uint64_t dx = depth_bits[x];
-        int j = i - 1;
-        while (j >= 0) {
-          const uint32_t y = vals[start + j];
-          const uint64_t dy = depth_bits[y];
-          if (!(dy > dx || (dy == dx && y > x))) break;
-          vals[start + j + 1] = y;
-          --j;
-        }
-        vals[start + j + 1] = x;
-      }
-    }
+    if (bad) repair_truncated_runs(vals + start, len, depth_bits, dmin, sh);
   }
 }
 
@@ -349,47 +364,18 @@ __global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restric
   const int t = blockIdx.x;
   const int start = ranges[2 * t], len = ranges[2 * t + 1] - start;
   const int sh = key_shift(depth_minmax, src_bits);
+  const uint64_t dmin = depth_minmax[0];
   if (!LARGE) {
     if (len <= 1 || len > 4096) return;
-    if (len <= 256) sort_bucket<NT, 2>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-    else if (len <= 512) sort_bucket<NT, 4>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-    else if (len <= 1024) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-    else if (len <= 2048) sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-    else sort_bucket<NT, 32>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
+    if (len <= 256) sort_bucket<NT, 2>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else if (len <= 512) sort_bucket<NT, 4>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else if (len <= 1024) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else if (len <= 2048) sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else sort_bucket<NT, 32>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
   } else {
     if (len <= 4096 || len > 16384) return;
-    if (len <= 8192) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-    else sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, sh, src_bits);
-  }
-}
-
-// Full-key fix-up after a truncated-key sort (see sort_bucket): checks adjacent
-// entries of a sorted bucket and, if any pair is out of (depth, source) order,
-// insertion-sorts the bucket by the full key (thread 0; only on near-equal depths).
-__device__ void fixup_full_order(uint32_t* __restrict__ vals, int len, const uint64_t* __restrict__ depth_bits) {
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i + 1 < len; i += blockDim.x) {
-    const uint32_t a = vals[i], b = vals[i + 1];
-    const uint64_t da = depth_bits[a], db = depth_bits[b];
-    if (da > db || (da == db && a > b)) bad = 1;
-  }
-  __syncthreads();
-  if (bad && threadIdx.x == 0) {
-    for (int i = 1; i < len; ++i) {
-      const uint32_t x = vals[i];
-      const uint64_t dx = depth_bits[x];
-      int j = i - 1;
-      while (j >= 0) {
-        const uint32_t y = vals[j];
-        const uint64_t dy = depth_bits[y];
-        if (!(dy > dx || (dy == dx && y > x))) break;
-        vals[j + 1] = y;
-        --j;
-      }
-      vals[j + 1] = x;
-    }
+    if (len <= 8192) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
   }
 }
 
@@ -458,9 +444,16 @@ __global__ void __launch_bounds__(1024) sort_tiles_huge_kernel(const int32_t* __
     dst = tmp;
   }
   const uint64_t smask = (1ull << src_bits) - 1ull;
-  for (int i = threadIdx.x; i < len; i += NT) tile_vals[start + i] = static_cast<uint32_t>(src[i] & smask);
+  const int sh = key_shift(depth_minmax, src_bits);
+  __shared__ int tie;
+  if (threadIdx.x == 0) tie = 0;
   __syncthreads();
-  if (key_shift(depth_minmax, src_bits) > 0) fixup_full_order(tile_vals + start, len, depth_bits);
+  for (int i = threadIdx.x; i < len; i += NT) {
+    tile_vals[start + i] = static_cast<uint32_t>(src[i] & smask);
+    if (sh > 0 && i + 1 < len && (src[i] >> src_bits) == (src[i + 1] >> src_bits)) tie = 1;
+  }
+  __syncthreads();
+  if (tie) repair_truncated_runs(tile_vals + start, len, depth_bits, depth_minmax[0], sh);
 }
 
 __global__ void compact_kernel(const int32_t* __restrict__ valid, const int32_t* __restrict__ pos,

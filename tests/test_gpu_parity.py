@@ -230,6 +230,7 @@ def test_gpu_huge_buckets_and_depth_ties(rend, count):
     rng = np.random.default_rng(count)
     cam = front_camera(48, 48, 60.0)
     z = rng.choice(np.linspace(2.0, 6.0, count // 4), size=count)  # every depth shared by ~4 surfels
+    z[::3] = np.nextafter(z[::3], np.inf)  # 1-ulp neighbours: equal truncated sort keys, different depths
     xy = rng.uniform(-0.02, 0.02, size=(count, 2)) * z[:, None]
     rows = np.zeros((count, 13))
     rows[:, 0:2] = xy
