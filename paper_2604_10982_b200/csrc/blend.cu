@@ -38,14 +38,52 @@ namespace {
 constexpr int kTile = 16;
 constexpr int kThreads = kTile * kTile;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 30;                   // records per warp chunk (30: the exp table fits 3 CTAs/SM)
 constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
 
-struct __align__(16) WarpStage {
-  SurfRec rec[2][kChunk];
-};
+// Kernel shape per Top-K width: records per warp chunk (double-buffered) and resident
+// CTAs per SM. Shared memory per CTA = 8 warps x 2 x chunk x 144 B of staged records
+// + the 2 KB exp table + the per-pixel Top-K lists (KMAX x 12 B per pixel); the
+// chunk is the largest that fits the residency (228 KB per SM, 1 KB reserved per
+// CTA) and the registers stay under 65536 / (256 x blocks).
+#ifndef PSM_BLEND_CH8
+#define PSM_BLEND_CH8 12
+#endif
+#ifndef PSM_BLEND_MB8
+#define PSM_BLEND_MB8 4
+#endif
+#ifndef PSM_BLEND_CH16
+#define PSM_BLEND_CH16 10
+#endif
+#ifndef PSM_BLEND_MB16
+#define PSM_BLEND_MB16 3
+#endif
+#ifndef PSM_BLEND_CH32
+#define PSM_BLEND_CH32 5
+#endif
+#ifndef PSM_BLEND_MB32
+#define PSM_BLEND_MB32 2
+#endif
+__host__ __device__ constexpr int chunk_for(int kmax) {
+  return kmax == 0 ? 30 : (kmax <= 8 ? PSM_BLEND_CH8 : (kmax <= 16 ? PSM_BLEND_CH16 : PSM_BLEND_CH32));
+}
+__host__ __device__ constexpr int min_blocks(int kmax) {
+  return kmax == 0 ? 3 : (kmax <= 8 ? PSM_BLEND_MB8 : (kmax <= 16 ? PSM_BLEND_MB16 : PSM_BLEND_MB32));
+}
+
+#ifdef PSM_BLEND_STATS
+// Instrumented build only (scratch profiling): work counters of the candidate loop.
+__device__ unsigned long long psm_blend_stats[16];
+#define PSM_STAT(i, v) atomicAdd(&psm_blend_stats[i], static_cast<unsigned long long>(v))
+#endif
+
 constexpr size_t kExpTabBytes = 256 * sizeof(uint64_t);
-constexpr size_t kSmemBytes = sizeof(WarpStage) * kWarps + kExpTabBytes;
+__host__ __device__ constexpr size_t stage_bytes(int kmax) { return static_cast<size_t>(kWarps) * 2 * chunk_for(kmax) * sizeof(SurfRec); }
+__host__ __device__ constexpr size_t smem_bytes(int kmax) {
+  return stage_bytes(kmax) + kExpTabBytes + static_cast<size_t>(kmax) * kThreads * (sizeof(double) + sizeof(int));
+}
+static_assert(smem_bytes(8) * PSM_BLEND_MB8 + 1024 * PSM_BLEND_MB8 <= 228 * 1024, "K=8 shape exceeds shared memory");
+static_assert(smem_bytes(16) * PSM_BLEND_MB16 + 1024 * PSM_BLEND_MB16 <= 228 * 1024, "K=16 shape exceeds shared memory");
+static_assert(smem_bytes(32) * PSM_BLEND_MB32 + 1024 * PSM_BLEND_MB32 <= 228 * 1024, "K=32 shape exceeds shared memory");
 
 // before(a, b) of topk_select (raster.cpp:232-235), proj order == source order.
 // Slots hold list positions; the source ids are only looked up on an exact weight tie.
@@ -124,15 +162,16 @@ __device__ __forceinline__ bool cull_meets(const SurfRec& r, float k, float x0, 
   return xl <= x1 && xr >= x0;
 }
 
-// Resident CTAs per SM: 3 (80 registers) for K <= 8, fewer for the wider register Top-K.
-constexpr int min_blocks(int kmax) { return kmax >= 32 ? 1 : (kmax >= 16 ? 2 : 3); }
-
 template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT>
 __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(BlendParams p) {
+  constexpr int kChunk = chunk_for(KMAX);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpStage& stage = reinterpret_cast<WarpStage*>(smem_raw)[threadIdx.x >> 5];
+  SurfRec* stage = reinterpret_cast<SurfRec*>(smem_raw) + (threadIdx.x >> 5) * 2 * kChunk;  // [2][kChunk]
   // psm_exp's 2^(i/128) table, one copy per CTA (random per-lane lookups: shared memory, not L1)
-  uint64_t* exp_tab = reinterpret_cast<uint64_t*>(smem_raw + sizeof(WarpStage) * kWarps);
+  uint64_t* exp_tab = reinterpret_cast<uint64_t*>(smem_raw + stage_bytes(KMAX));
+  // per-pixel Top-K lists (slot-major: [slot][thread], conflict-free): weights and list positions
+  double* top_w = reinterpret_cast<double*>(exp_tab + 256);
+  int* top_p = reinterpret_cast<int*>(top_w + KMAX * kThreads);
   exp_tab[threadIdx.x] = psm_exp_tab_dev[threadIdx.x];
   __syncthreads();
 
@@ -160,12 +199,16 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   bool done = !inside;
   float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
   double exp_depth = 0, dom_depth = 0, dom_w = 0;
-  double sw[KMAX > 0 ? KMAX : 1];
-  int ss[KMAX > 0 ? KMAX : 1];
-#pragma unroll
-  for (int i = 0; i < (KMAX > 0 ? KMAX : 1); ++i) {
-    sw[i] = -1.0;
-    ss[i] = 0;  // list position; never compared (weights are > 0)
+  // Top-K: the k_sel best (weight desc, source asc) so far live in shared memory; the
+  // registers only hold the admission threshold (the k_sel-th entry).
+  const int klen = p.k_sel < 1 ? 1 : p.k_sel;
+  double thr_w = -1.0;  // weights are > 0: the first k_sel contributors always enter
+  int thr_p = 0;        // list position; never compared while thr_w < 0
+  if constexpr (KMAX > 0) {
+    for (int i = 0; i < klen; ++i) {
+      top_w[i * kThreads + tid] = -1.0;
+      top_p[i * kThreads + tid] = 0;
+    }
   }
 
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
@@ -174,13 +217,16 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
     if (lane < kChunk && base + lane < end) {
       const int s = static_cast<int>(__ldg(p.vals + base + lane));
       const char* g = reinterpret_cast<const char*>(p.recs + s);
-      char* d = reinterpret_cast<char*>(&stage.rec[buf][lane]);
+      char* d = reinterpret_cast<char*>(stage + buf * kChunk + lane);
 #pragma unroll
       for (int k = 0; k < kRecVec; ++k) cp_async16(d + 16 * k, g + 16 * k);
     }
     cp_async_commit();
   };
 
+#ifdef PSM_BLEND_STATS
+  unsigned st_iter = 0, st_sup = 0, st_alpha = 0, st_chunks = 0, st_streamed = 0, st_live = 0, st_any_sup = 0;
+#endif
   if (__any_sync(0xffffffffu, !done) && start < end) prefetch(start, 0);
   int buf = 0;
   for (int base = start; base < end; base += kChunk, buf ^= 1) {
@@ -193,15 +239,31 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
       cp_async_wait<0>();
     }
     __syncwarp();
-    const SurfRec* recs = stage.rec[buf];
+    const SurfRec* recs = stage + buf * kChunk;
     // candidates that reach no pixel centre of this warp's block are skipped as a whole
     unsigned live = (1u << cnt) - 1u;  // cnt <= 30
     if (p.support_cutoff) live = __ballot_sync(0xffffffffu, lane < cnt && cull_meets(recs[lane], kcull, bx0, bx1, by0, by1));
+#ifdef PSM_BLEND_STATS
+    st_chunks++;
+    st_streamed += cnt;
+    st_live += __popc(live);
+#endif
     if (!done) {
       while (live) {
         const int j = __ffs(live) - 1;
         live &= live - 1;
         const SurfRec& r = recs[j];
+#ifdef PSM_BLEND_STATS
+        st_iter++;
+        {
+          const double dx = px - r.cx, dy = py - r.cy;
+          const bool sp = !p.support_cutoff || !(r.f00 * dx * dx + r.f01x2 * dx * dy + r.f11 * dy * dy > p.chi2);
+          const unsigned am = __activemask();
+          const unsigned bm = __ballot_sync(am, sp);
+          if (sp) st_sup++;
+          if (lane == __ffs(am) - 1 && bm) st_any_sup++;
+        }
+#endif
         if (p.support_cutoff) {
           const double dx = px - r.cx;
           const double dy = py - r.cy;
@@ -215,6 +277,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
         const double u = w0 * rcp, v = w1 * rcp;
         const double alpha = r.opacity * psm_exp_t(-0.5 * (u * u + v * v), exp_tab);
         if (alpha < p.alpha_min || alpha <= 0.0) continue;
+#ifdef PSM_BLEND_STATS
+        st_alpha++;
+#endif
         const double wt = alpha * T;
         // colour / depth / normal always over the full list (raster.cpp:405-436)
         const float wf = static_cast<float>(wt);
@@ -231,19 +296,20 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
         }
         const int pos = base + j;  // list position; source id = vals[pos]
         if constexpr (KMAX > 0) {
-          if (before(wt, pos, sw[KMAX - 1], ss[KMAX - 1], p.vals)) {
-#pragma unroll
-            for (int i = KMAX - 1; i > 0; --i) {
-              if (before(wt, pos, sw[i], ss[i], p.vals)) {
-                const bool above_prev = before(wt, pos, sw[i - 1], ss[i - 1], p.vals);
-                sw[i] = above_prev ? sw[i - 1] : wt;
-                ss[i] = above_prev ? ss[i - 1] : pos;
-              }
+          if (before(wt, pos, thr_w, thr_p, p.vals)) {  // insertion select (raster.cpp:238-249)
+            int i = klen - 1;
+            while (i > 0) {
+              const double w = top_w[(i - 1) * kThreads + tid];
+              const int q = top_p[(i - 1) * kThreads + tid];
+              if (!before(wt, pos, w, q, p.vals)) break;
+              top_w[i * kThreads + tid] = w;
+              top_p[i * kThreads + tid] = q;
+              --i;
             }
-            if (before(wt, pos, sw[0], ss[0], p.vals)) {
-              sw[0] = wt;
-              ss[0] = pos;
-            }
+            top_w[i * kThreads + tid] = wt;
+            top_p[i * kThreads + tid] = pos;
+            thr_w = top_w[(klen - 1) * kThreads + tid];
+            thr_p = top_p[(klen - 1) * kThreads + tid];
           }
         }
         if constexpr (FULL_LIST) {
@@ -260,11 +326,24 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
     __syncwarp();  // the buffer is refilled by the next iteration's prefetch
   }
   cp_async_wait<0>();
-
-  if constexpr (KMAX > 0) {
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i) ss[i] = sw[i] > 0.0 ? static_cast<int>(__ldg(p.vals + ss[i])) : -1;
+#ifdef PSM_BLEND_STATS
+  {
+    unsigned mx = st_iter;
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    PSM_STAT(0, st_iter);
+    PSM_STAT(1, st_sup);
+    PSM_STAT(2, st_alpha);
+    PSM_STAT(6, st_any_sup);
+    if (lane == 0) {
+      PSM_STAT(3, mx);
+      PSM_STAT(4, st_chunks);
+      PSM_STAT(5, st_streamed);
+      PSM_STAT(7, st_live);
+      PSM_STAT(8, 1);
+    }
   }
+#endif
+
   const int k_sel = p.k_sel;
   int blend_n = m;
   if constexpr (KMAX > 0) blend_n = m < k_sel ? m : k_sel;
@@ -282,9 +361,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
     p.blend_count[pix] = m;
     if constexpr (KMAX > 0) {
       if (p.topk_dbg) {
-#pragma unroll
-        for (int i = 0; i < KMAX; ++i)
-          if (i < k_sel) p.topk_dbg[pix * k_sel + i] = i < blend_n ? ss[i] : -1;
+        for (int i = 0; i < k_sel; ++i)
+          p.topk_dbg[pix * k_sel + i] =
+              i < blend_n ? static_cast<int>(__ldg(p.vals + top_p[i * kThreads + tid])) : -1;
       }
     }
     if constexpr (FULL_LIST) {
@@ -310,9 +389,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
     constexpr int PPI = 32 / LPP;
     const int D = p.feat_dims;
     const int grp = lane / LPP, sub = lane % LPP;
-    float swf[KMAX > 0 ? KMAX : 1];
-#pragma unroll
-    for (int i = 0; i < (KMAX > 0 ? KMAX : 1); ++i) swf[i] = static_cast<float>(sw[i]);
     const bool only_sem = p.n_q == 0;
     for (int q0 = 0; q0 < 32; q0 += PPI) {
       const int q = q0 + grp;
@@ -330,11 +406,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
         for (int e = 0; e < VEC; ++e) acc[v][e] = 0.f;
       using TV = typename FVec<VEC>::T;
       if constexpr (KMAX > 0) {
-#pragma unroll
-        for (int i = 0; i < KMAX; ++i) {
-          const int s = __shfl_sync(0xffffffffu, ss[i], q);
-          const float w = __shfl_sync(0xffffffffu, swf[i], q);
-          if (i < nq) {
+        const int qt = (tid & ~31) + q;  // the pixel's thread: its Top-K list column
+        for (int i = 0; i < nq; ++i) {
+          {
+            const int s = static_cast<int>(__ldg(p.vals + top_p[i * kThreads + qt]));
+            const float w = static_cast<float>(top_w[i * kThreads + qt]);
             const TV* row = reinterpret_cast<const TV*>(p.feat + static_cast<int64_t>(s) * D);
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
@@ -420,10 +496,10 @@ void launch_t(const BlendParams& p, int tiles, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured >> dev & 1ull)) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_bytes(KMAX)));
     configured |= 1ull << dev;
   }
-  kern<<<tiles, kThreads, kSmemBytes, st>>>(p);
+  kern<<<tiles, kThreads, smem_bytes(KMAX), st>>>(p);
 }
 
 // Feature-lane shapes: float4 lanes, 32/LPP pixels per warp iteration for the
@@ -448,6 +524,17 @@ void launch_feat(const BlendParams& p, int tiles, cudaStream_t st) {
 }
 
 }  // namespace
+
+#ifdef PSM_BLEND_STATS
+extern "C" void psm_blend_stats_read(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, psm_blend_stats, sizeof(psm_blend_stats));
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(psm_blend_stats, z, sizeof(z));
+  }
+}
+#endif
 
 int blend_kmax_for(int k_sel) {
   if (k_sel <= 8) return 8;

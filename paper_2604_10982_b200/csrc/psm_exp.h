@@ -106,14 +106,28 @@ PSM_HD double psm_exp_special(double tmp, uint64_t sbits, uint64_t ki) {
   return 0x1p-1022 * y;
 }
 
+// Device: the polynomial / reduction constants live in the constant bank, so the
+// fp64 instructions take them as c[] operands instead of re-materialising each
+// 64-bit immediate into registers on every call.
+#if defined(__CUDACC__)
+static __constant__ double psm_exp_kc[8] = {0x1.71547652b82fep7, 0x1.8p52, -0x1.62e42fefa0000p-8,
+                                            -0x1.cf79abc9e3b3ap-47, 0x1.ffffffffffdbdp-2, 0x1.555555555543cp-3,
+                                            0x1.55555cf172b91p-5, 0x1.1111167a4d017p-7};
+#endif
+#if defined(__CUDA_ARCH__)
+#define PSM_EXPK(i, lit) psm_exp_kc[i]
+#else
+#define PSM_EXPK(i, lit) (lit)
+#endif
+
 // `tab` is the 256-word table (psm_exp_tab_dev, a shared-memory copy of it, or the host array).
 PSM_HD double psm_exp_t(double x, const uint64_t* tab) {
-  const double kInvLn2N = 0x1.71547652b82fep7;   // 128 / ln2
+  const double kInvLn2N = PSM_EXPK(0, 0x1.71547652b82fep7);  // 128 / ln2
   const double kShift = 0x1.8p52;
-  const double kNegLn2HiN = -0x1.62e42fefa0000p-8;
-  const double kNegLn2LoN = -0x1.cf79abc9e3b3ap-47;
-  const double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
-  const double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+  const double kNegLn2HiN = PSM_EXPK(2, -0x1.62e42fefa0000p-8);
+  const double kNegLn2LoN = PSM_EXPK(3, -0x1.cf79abc9e3b3ap-47);
+  const double C2 = PSM_EXPK(4, 0x1.ffffffffffdbdp-2), C3 = PSM_EXPK(5, 0x1.555555555543cp-3);
+  const double C4 = PSM_EXPK(6, 0x1.55555cf172b91p-5), C5 = PSM_EXPK(7, 0x1.1111167a4d017p-7);
   const uint64_t ix = psm_double_to_bits(x);
   uint32_t abstop = static_cast<uint32_t>(ix >> 52) & 0x7ffu;
   if (abstop - 0x3c9u >= 0x3fu) {                      // |x| < 2^-54, |x| >= 512, inf or nan
