@@ -202,14 +202,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   // Top-K: the k_sel best (weight desc, source asc) so far live in shared memory; the
   // registers only hold the admission threshold (the k_sel-th entry).
   const int klen = p.k_sel < 1 ? 1 : p.k_sel;
+  int n_top = 0;  // filled entries
   double thr_w = -1.0;  // weights are > 0: the first k_sel contributors always enter
   int thr_p = 0;        // list position; never compared while thr_w < 0
-  if constexpr (KMAX > 0) {
-    for (int i = 0; i < klen; ++i) {
-      top_w[i * kThreads + tid] = -1.0;
-      top_p[i * kThreads + tid] = 0;
-    }
-  }
 
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
   const float kcull = static_cast<float>(p.chi2) * 1.0001f;
@@ -297,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
         const int pos = base + j;  // list position; source id = vals[pos]
         if constexpr (KMAX > 0) {
           if (before(wt, pos, thr_w, thr_p, p.vals)) {  // insertion select (raster.cpp:238-249)
-            int i = klen - 1;
+            int i = n_top < klen ? n_top++ : klen - 1;  // the list fills without a threshold
             while (i > 0) {
               const double w = top_w[(i - 1) * kThreads + tid];
               const int q = top_p[(i - 1) * kThreads + tid];
@@ -308,8 +303,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
             }
             top_w[i * kThreads + tid] = wt;
             top_p[i * kThreads + tid] = pos;
-            thr_w = top_w[(klen - 1) * kThreads + tid];
-            thr_p = top_p[(klen - 1) * kThreads + tid];
+            if (n_top == klen) {
+              thr_w = top_w[(klen - 1) * kThreads + tid];
+              thr_p = top_p[(klen - 1) * kThreads + tid];
+            }
           }
         }
         if constexpr (FULL_LIST) {
