@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   exp_tab[threadIdx.x] = psm_exp_tab_dev[threadIdx.x];
   __syncthreads();
 
-  const int tile = blockIdx.x;
+  const int tile = p.tile_base + static_cast<int>(blockIdx.x);
   const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;

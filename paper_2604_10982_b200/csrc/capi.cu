@@ -15,6 +15,7 @@
 // point returns PSM_ECUDA.
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -49,6 +50,9 @@ struct psm_ctx {
   bool own_stream = false;
   cudaStream_t side = nullptr;   // concurrent side work within a frame (large tile buckets)
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t copy = nullptr;   // device-to-host copies of finished row bands (host targets)
+  cudaEvent_t band_ev[8] = {};
+  cudaEvent_t copy_done = nullptr;
   std::string err;
   bool profiling = false;
   cudaEvent_t ev[8] = {};
@@ -151,8 +155,14 @@ int check_config(psm_ctx* ctx, const psm_raster_config* cfg, int feat_dims) {
 // frame whose RN-Total outgrew the key buffers), which reads RN-Total to size
 // them; frames after that run without a host sync. Leaves results in `pl`
 // (device) and counters in the pinned ctx->h_small (valid after the stream syncs).
+// Host-target frames pass `on_band`: the blend then runs as row bands of tiles and
+// on_band(band, y0, y1) is called after each band's launch (it queues that band's
+// device-to-host copies on the copy stream, overlapping the next band's blend).
+using BandHook = std::function<int(int band, int y0, int y1)>;
+constexpr int kHostBands = 4;
+
 int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
-                const Planes& pl, psm_debug* dbg) {
+                const Planes& pl, psm_debug* dbg, const BandHook* on_band = nullptr) {
   cudaStream_t st = ctx->stream;
   const int64_t n = sc->n;
   const int W = cam->width, H = cam->height;
@@ -286,8 +296,19 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     bp.lists = lists;
     bp.list_cap = ctx->list_cap;
   }
-  launch_blend(bp, tiles, topk, st);
-  PSM_CUDA_TRY(cudaGetLastError());
+  if (!on_band) {
+    launch_blend(bp, tiles, topk, st);
+    PSM_CUDA_TRY(cudaGetLastError());
+  } else {
+    const int bands = tiles_y < kHostBands ? tiles_y : kHostBands;
+    for (int b = 0; b < bands; ++b) {
+      const int ty0 = tiles_y * b / bands, ty1 = tiles_y * (b + 1) / bands;
+      bp.tile_base = ty0 * tiles_x;
+      launch_blend(bp, (ty1 - ty0) * tiles_x, topk, st);
+      PSM_CUDA_TRY(cudaGetLastError());
+      PSM_TRY((*on_band)(b, ty0 * ts, ty1 * ts < H ? ty1 * ts : H));
+    }
+  }
   record(ctx, 5);
 
   // counters -> pinned host memory (read after the stream syncs)
@@ -413,25 +434,36 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
   // feature planes are always produced (context scratch when the caller passes NULL)
   if (cs > 0) PSM_TRY(pick(tg->sem_feat, ctx->plane_sem, npx * cs, 4, reinterpret_cast<void**>(&pl.sem)));
   if (nq > 0) PSM_TRY(pick(tg->ins_dist, ctx->plane_ins, npx * nq, 4, reinterpret_cast<void**>(&pl.ins)));
-  auto enqueue_d2h = [&]() -> int {
-    if (tg->on_device) return PSM_OK;
-    cudaStream_t st = ctx->stream;
-    auto d2h = [&](void* dst, const void* src, size_t bytes) -> int {
-      if (dst) PSM_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+  // host targets: each finished row band of every plane is copied on the copy stream while
+  // the next band blends; the main stream then waits for the copies (the planes are
+  // context scratch that the next frame overwrites)
+  const BandHook band_d2h = [&](int b, int y0, int y1) -> int {
+    cudaStream_t cs_ = ctx->copy;
+    PSM_CUDA_TRY(cudaEventRecord(ctx->band_ev[b], ctx->stream));
+    PSM_CUDA_TRY(cudaStreamWaitEvent(cs_, ctx->band_ev[b], 0));
+    const size_t p0 = static_cast<size_t>(y0) * cam->width, np = static_cast<size_t>(y1 - y0) * cam->width;
+    auto d2h = [&](void* dst, const void* src, size_t ch) -> int {
+      if (dst && np)
+        PSM_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dst) + p0 * ch * 4, static_cast<const char*>(src) + p0 * ch * 4,
+                                     np * ch * 4, cudaMemcpyDeviceToHost, cs_));
       return PSM_OK;
     };
-    PSM_TRY(d2h(tg->color, pl.color, npx * 12));
-    PSM_TRY(d2h(tg->depth, pl.depth, npx * 8));
-    PSM_TRY(d2h(tg->normal, pl.normal, npx * 12));
-    PSM_TRY(d2h(tg->alpha_acc, pl.alpha, npx * 4));
-    PSM_TRY(d2h(tg->ins_argmax, pl.arg, npx * 4));
-    PSM_TRY(d2h(tg->blend_count, pl.cnt, npx * 4));
-    if (pl.sem && tg->sem_feat) PSM_TRY(d2h(tg->sem_feat, pl.sem, npx * cs * 4));
-    if (pl.ins && tg->ins_dist) PSM_TRY(d2h(tg->ins_dist, pl.ins, npx * nq * 4));
+    PSM_TRY(d2h(tg->color, pl.color, 3));
+    PSM_TRY(d2h(tg->depth, pl.depth, 2));
+    PSM_TRY(d2h(tg->normal, pl.normal, 3));
+    PSM_TRY(d2h(tg->alpha_acc, pl.alpha, 1));
+    PSM_TRY(d2h(tg->ins_argmax, pl.arg, 1));
+    PSM_TRY(d2h(tg->blend_count, pl.cnt, 1));
+    if (pl.sem && tg->sem_feat) PSM_TRY(d2h(tg->sem_feat, pl.sem, cs));
+    if (pl.ins && tg->ins_dist) PSM_TRY(d2h(tg->ins_dist, pl.ins, nq));
+    if (y1 == cam->height) {
+      PSM_CUDA_TRY(cudaEventRecord(ctx->copy_done, cs_));
+      PSM_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->copy_done, 0));
+    }
     return PSM_OK;
   };
-  PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg));
-  PSM_TRY(enqueue_d2h());
+  const BandHook* hook = tg->on_device ? nullptr : &band_d2h;
+  PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg, hook));
   if (counters || !tg->on_device || ctx->profiling || dbg) {
     for (int attempt = 0;; ++attempt) {
       PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -439,8 +471,7 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
       PSM_TRY(check_frame(ctx, &rerun));
       if (!rerun) break;
       if (attempt >= 3) return fail(ctx, PSM_ENOMEM, "render buffers did not converge");
-      PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg));
-      PSM_TRY(enqueue_d2h());
+      PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg, hook));
     }
     ctx->pend_valid = false;
     finish_counters(ctx);
@@ -508,6 +539,13 @@ int psm_create(int device, void* stream, psm_ctx** out) {
     delete ctx;
     return PSM_ECUDA;
   }
+  if (cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming) != cudaSuccess) {
+    delete ctx;
+    return PSM_ECUDA;
+  }
+  for (auto& e : ctx->band_ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { delete ctx; return PSM_ECUDA; }
   if (cudaMallocHost(&ctx->h_small, 8 * sizeof(int64_t)) != cudaSuccess) { delete ctx; return PSM_ENOMEM; }
   std::memset(ctx->h_small, 0, 8 * sizeof(int64_t));
   *out = ctx;
@@ -529,6 +567,9 @@ int psm_destroy(psm_ctx* ctx) {
   if (ctx->fork) cudaEventDestroy(ctx->fork);
   if (ctx->join) cudaEventDestroy(ctx->join);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  for (auto& e : ctx->band_ev) if (e) cudaEventDestroy(e);
+  if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

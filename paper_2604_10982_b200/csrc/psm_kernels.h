@@ -16,6 +16,7 @@ struct BlendParams {
   const float* feat;      // [N][feat_dims]: f_sem | labels, fp32
   int32_t feat_dims, c_sem, n_q;
   int32_t width, height, tiles_x;
+  int32_t tile_base;      // first tile of this launch (row bands: blockIdx.x + tile_base)
   double cam_cx, cam_cy, cam_fx, cam_fy;
   double chi2, alpha_min, t_min, bg0, bg1, bg2;
   int32_t support_cutoff, render_depth_normal, k_sel;
