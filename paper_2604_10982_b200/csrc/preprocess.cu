@@ -160,11 +160,11 @@ __device__ __forceinline__ bool project_one(int64_t i, const double* __restrict_
     const double dx = sqrt(rs.chi2 * F00), dy = sqrt(rs.chi2 * F11);
     x0 = cx - dx; x1 = cx + dx; y0 = cy - dy; y1 = cy + dy;
   }
-  const double ts = rs.tile_size;
-  b.tx0 = max(x86_cvt(floor(x0 / ts)), 0);
-  b.tx1 = min(x86_cvt(floor(x1 / ts)), rs.tiles_x - 1);
-  b.ty0 = max(x86_cvt(floor(y0 / ts)), 0);
-  b.ty1 = min(x86_cvt(floor(y1 / ts)), rs.tiles_y - 1);
+  const int ts = rs.tile_size;  // floor(x / ts) as raster.cpp:62-65 (exact reciprocal for 16)
+  b.tx0 = max(x86_cvt(floor(psm_div_tile(x0, ts))), 0);
+  b.tx1 = min(x86_cvt(floor(psm_div_tile(x1, ts))), rs.tiles_x - 1);
+  b.ty0 = max(x86_cvt(floor(psm_div_tile(y0, ts))), 0);
+  b.ty1 = min(x86_cvt(floor(psm_div_tile(y1, ts))), rs.tiles_y - 1);
   b.pad0 = b.pad1 = 0;
   bins[i] = b;
   depth_bits[i] = static_cast<uint64_t>(__double_as_longlong(zz));

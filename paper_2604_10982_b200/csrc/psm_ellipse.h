@@ -28,6 +28,10 @@
 #include <math.h>
 #endif
 
+// x / ts. For a power-of-two tile size the quotient is exact-scaled, so multiplying by
+// the (exact) reciprocal gives the identical double without a division.
+PSM_EHD double psm_div_tile(double x, int ts) { return (ts & (ts - 1)) == 0 ? x * (1.0 / ts) : x / ts; }
+
 // Per-surfel constants of the row test (computed once per surfel, used per tile row).
 struct PsmEllipse {
   double cx, cy;
@@ -86,8 +90,8 @@ PSM_EHD int psm_ellipse_row(const PsmEllipse& e, int ty, int ts, int height, int
   const double xr = e.cx + e.slope * dr + sqrt(rr * e.q) + 1e-3;
   const double xl = e.cx + e.slope * dl - sqrt(rl * e.q) - 1e-3;
   // tiles whose pixel-centre span [tx*ts + 0.5, tx*ts + ts - 0.5] meets [xl, xr]
-  double lo = ceil((xl - (ts - 0.5)) / ts);
-  double hi = floor((xr - 0.5) / ts);
+  double lo = ceil(psm_div_tile(xl - (ts - 0.5), ts));
+  double hi = floor(psm_div_tile(xr - 0.5, ts));
   if (!(lo == lo) || !(hi == hi)) {  // NaN anywhere: keep the AABB row
     lo = ax0;
     hi = ax1;
