@@ -322,8 +322,9 @@ def run_ours(args):
                      "peak_source": peak_src, "alg_bytes_per_launch": b_blend, "launch_ms": blend_avg},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 5 * args.steps,
-        "gpu_launches_note": "per step: preprocess, tile_scan, emit, sort_tiles, blend (+2 memsets)",
+        "gpu_launches": 8 * args.steps,
+        "gpu_launches_note": "per step: preprocess, tile_sub_scan, tile_scan, emit, sort_tiles<1024>, "
+                             "sort_tiles_huge, sort_tiles<128>, blend (+3 memsets, 1 small H2D)",
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
