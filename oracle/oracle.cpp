@@ -15,6 +15,8 @@
 //   src/math_util.cpp:16-23,46-52   rotation_unit, rotation_from_quat
 //   src/math_util.cpp:135-162       worker_count, parallel_chunks
 //   include/psimap/core_types.hpp:51-52  Camera::to_camera, center_world
+//   src/panoptic.cpp:36-91   assign_labels (math in psm_panoptic.h, shared with the GPU)
+//   src/metrics.cpp:339-369  render_panoptic epilogue (oracle/pyoracle.py, over render's fp64 planes)
 //
 // Why a restatement: the reference needs Eigen3, which is not in this image
 // (proj/CMakeLists.txt:13-15 `find_path(EIGEN3_INCLUDE_DIR ... REQUIRED)`), so
@@ -45,6 +47,7 @@
 #include "../include/psm.h"
 #include "../paper_2604_10982_b200/csrc/psm_ellipse.h"
 #include "../paper_2604_10982_b200/csrc/psm_exp.h"
+#include "../paper_2604_10982_b200/csrc/psm_panoptic.h"
 
 namespace {
 
@@ -455,6 +458,41 @@ int oracle_bin(const double* surfels13, int64_t n, const psm_camera* pcam, const
     counters->blended_total = 0;
   }
   return PSM_OK;
+}
+
+// assign_labels (panoptic.cpp:36-91). surfels13: N x 13 (centre = columns 0..2);
+// f_ins: N x c_ins; queries: feat [n_queries x c_ins], mean [n_queries x 3], cov
+// [n_queries x 9] column-major, alive flags. dist_out: N x n_queries (per-surfel
+// contiguous, the MatX column of surfel s); argmax_out: N (query index, -1 when no
+// query is alive). Parallel over surfels; each surfel is independent.
+void oracle_assign_labels(const double* surfels13, int64_t n, const double* f_ins, int32_t c_ins, int32_t n_queries,
+                          const double* q_feat, const double* q_mean, const double* q_cov, const int32_t* q_alive,
+                          double* dist_out, int32_t* argmax_out, int32_t threads) {
+  std::vector<int> alive;
+  for (int q = 0; q < n_queries; ++q)
+    if (q_alive[q]) alive.push_back(q);
+  const int na = static_cast<int>(alive.size());
+  std::vector<double> fq(static_cast<size_t>(na) * c_ins), mean(3 * na), inv(9 * na);
+  for (int a = 0; a < na; ++a) {
+    for (int c = 0; c < c_ins; ++c) fq[a * c_ins + c] = q_feat[static_cast<int64_t>(alive[a]) * c_ins + c];
+    for (int i = 0; i < 3; ++i) mean[a * 3 + i] = q_mean[alive[a] * 3 + i];
+    psm_query_inverse(q_cov + alive[a] * 9, inv.data() + a * 9);
+  }
+  parallel_chunks(n, threads, [&](int64_t b, int64_t e) {
+    std::vector<double> av(na > 0 ? na : 1);
+    for (int64_t s = b; s < e; ++s) {
+      double* row = dist_out + s * n_queries;
+      for (int q = 0; q < n_queries; ++q) row[q] = 0.0;
+      if (na == 0) {
+        argmax_out[s] = -1;
+        continue;
+      }
+      const int best = psm_assign_one(f_ins + s * c_ins, c_ins, surfels13 + s * 13, na, fq.data(), mean.data(),
+                                      inv.data(), av.data(), 1, psm_exp_tab_host);
+      for (int a = 0; a < na; ++a) row[alive[a]] = av[a];
+      argmax_out[s] = alive[best];
+    }
+  });
 }
 
 // psm_exp itself, vectorised, for the libm-substitution pin.

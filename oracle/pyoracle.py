@@ -251,3 +251,36 @@ def render_cache(scene, labels, cam, cfg) -> dict:
        _p(color), _p(sem), _p(arg), _p(cnt), C.byref(cache))
     return {"color": color, "sem_feat": sem, "ins_argmax": arg, "blend_count": cnt, "offsets": offs,
             "src": src[:total], "alpha": alpha[:total]}
+
+
+def assign_labels(surfels13, f_ins, queries, threads: int = 0):
+    """assign_labels (panoptic.cpp:36-91) on the oracle: (dist (N, Q) per-surfel rows, argmax (N,))."""
+    from paper_2604_10982_b200.panoptic import pack_queries
+    lib = load()
+    fn = lib.oracle_assign_labels
+    fn.restype = None
+    vp = C.c_void_p
+    fn.argtypes = [vp, C.c_int64, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp, C.c_int32]
+    s = np.ascontiguousarray(np.asarray(surfels13, dtype=np.float64).reshape(-1, 13))
+    n = s.shape[0]
+    f = np.ascontiguousarray(np.asarray(f_ins, dtype=np.float64).reshape(n, -1))
+    c_ins = f.shape[1]
+    feat, mean, cov, alive, _ = pack_queries(queries, c_ins)
+    q = len(queries)
+    dist = np.zeros((n, q))
+    arg = np.full(n, -1, np.int32)
+    if n:
+        fn(_p(s), n, _p(f), c_ins, q, _p(feat), _p(mean), _p(cov), _p(alive), _p(dist), _p(arg), threads)
+    return dist, arg
+
+
+def render_panoptic(scene, f_ins, queries, cam, cfg) -> dict:
+    """render_panoptic (metrics.cpp:339-369): assign_labels, render with the label
+    distribution, then the per-pixel epilogue over the fp64 planes."""
+    from paper_2604_10982_b200.panoptic import panoptic_epilogue
+    dist, arg = assign_labels(scene.surfels, f_ins, queries)
+    labels = dist if len(queries) else None
+    out = render(scene, labels, cam, cfg)
+    pr = panoptic_epilogue(out["alpha_acc"], out["ins_argmax"], out["sem_feat"], [q.class_id for q in queries])
+    out.update(ids=pr.ids, classes=pr.classes, sem_classes=pr.sem_classes, dist=dist, label_argmax=arg)
+    return out

@@ -1,0 +1,132 @@
+// psm_panoptic.h — the panoptic label assignment of Ψ-Map, shared verbatim by the
+// CUDA kernel (labels.cu) and the CPU oracle so both produce the same bits.
+//
+// assign_labels (proj/src/panoptic.cpp:36-91): for every surfel s and alive query a
+//   A(a, s) = sigmoid(f_q(a) . f_ins(s)) * exp(-1/2 d^T Sigma_a^-1 d),  d = mu_s - mean_a
+// (attention_map, panoptic.cpp:32-34), then a softmax over the alive queries,
+//   dist(a, s) = exp(A - A_max) / sum_b exp(A_b - A_max),
+// and argmax(s) = the first alive query with the largest A (ties to the lower index).
+// Dead queries keep dist 0. Sigma_a^-1 comes from an LLT of the symmetrised
+// covariance, retried with an eps*I floor when it is not positive definite
+// (panoptic.cpp:53-62).
+//
+// Evaluation order: dot products and 3x3 products are left-to-right sums; the LLT is
+// Eigen's unblocked lower algorithm (llt_inplace::unblocked) with its solve against
+// the identity. Eigen's own vectorised reductions may associate differently, so the
+// agreement with an Eigen build of the reference is tolerance-level (pinned by
+// test_panoptic.cpp:86-183, ported in tests/test_panoptic_oracle.py); GPU and oracle
+// agree bit for bit. exp is psm_exp (glibc-exact); compile without contraction.
+#ifndef PSM_PANOPTIC_H
+#define PSM_PANOPTIC_H
+
+#include <stdint.h>
+
+#include "psm_exp.h"
+
+#if defined(__CUDACC__)
+#define PSM_PHD __host__ __device__ __forceinline__
+#else
+#define PSM_PHD static inline
+#include <math.h>
+#endif
+
+// sigmoid (math_util.cpp:122-128)
+PSM_PHD double psm_sigmoid_t(double x, const uint64_t* tab) {
+  if (x >= 0) return 1.0 / (1.0 + psm_exp_t(-x, tab));
+  const double e = psm_exp_t(x, tab);
+  return e / (1.0 + e);
+}
+
+// Lower Cholesky of a symmetric 3x3 (column-major a[c*3 + r]); 0 if not positive definite.
+PSM_PHD int psm_llt3(const double* a, double* l) {
+  for (int i = 0; i < 9; ++i) l[i] = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    double x = a[k * 3 + k];
+    if (k == 1) x -= l[0 * 3 + 1] * l[0 * 3 + 1];
+    if (k == 2) x -= l[0 * 3 + 2] * l[0 * 3 + 2] + l[1 * 3 + 2] * l[1 * 3 + 2];
+    if (!(x > 0.0)) return 0;
+    x = sqrt(x);
+    l[k * 3 + k] = x;
+    for (int i = k + 1; i < 3; ++i) {
+      double v = a[k * 3 + i];
+      if (k == 1) v -= l[0 * 3 + i] * l[0 * 3 + 1];
+      if (k == 2) v -= l[0 * 3 + i] * l[0 * 3 + 2] + l[1 * 3 + i] * l[1 * 3 + 2];
+      l[k * 3 + i] = v / x;
+    }
+  }
+  return 1;
+}
+
+// X = (L L^T)^-1 by forward then backward substitution against the identity.
+PSM_PHD void psm_llt3_inverse(const double* l, double* inv) {
+  const double l00 = l[0], l10 = l[1], l20 = l[2], l11 = l[4], l21 = l[5], l22 = l[8];
+  for (int c = 0; c < 3; ++c) {
+    const double e0 = c == 0 ? 1.0 : 0.0, e1 = c == 1 ? 1.0 : 0.0, e2 = c == 2 ? 1.0 : 0.0;
+    const double y0 = e0 / l00;
+    const double y1 = (e1 - l10 * y0) / l11;
+    const double y2 = (e2 - l20 * y0 - l21 * y1) / l22;
+    const double x2 = y2 / l22;
+    const double x1 = (y1 - l21 * x2) / l11;
+    const double x0 = (y0 - l10 * x1 - l20 * x2) / l00;
+    inv[c * 3 + 0] = x0;
+    inv[c * 3 + 1] = x1;
+    inv[c * 3 + 2] = x2;
+  }
+}
+
+// Sigma^-1 of a query covariance (panoptic.cpp:53-62), column-major in and out.
+PSM_PHD void psm_query_inverse(const double* cov, double* inv) {
+  double s[9], l[9];
+  for (int c = 0; c < 3; ++c)
+    for (int r = 0; r < 3; ++r) s[c * 3 + r] = 0.5 * (cov[c * 3 + r] + cov[r * 3 + c]);
+  if (!psm_llt3(s, l)) {
+    const double tr = (s[0] + s[4]) + s[8];
+    const double eps = 1e-8 * (tr > 1e-12 ? tr : 1e-12);
+    s[0] += eps;
+    s[4] += eps;
+    s[8] += eps;
+    psm_llt3(s, l);  // as the reference, the retry's outcome is used unchecked
+  }
+  psm_llt3_inverse(l, inv);
+}
+
+// One surfel against the n_alive alive queries: fq[a * c_ins + c], mean[a * 3 + i],
+// inv[a * 9 + c * 3 + r] (column-major). Writes A to a_vals[a * a_stride] and then the
+// softmax probability over it (in place); returns the argmax among the alive queries.
+PSM_PHD int psm_assign_one(const double* f_ins, int c_ins, const double* center, int n_alive, const double* fq,
+                           const double* mean, const double* inv, double* a_vals, int a_stride,
+                           const uint64_t* tab) {
+  double a_max = -1;
+  for (int a = 0; a < n_alive; ++a) {
+    double dot = 0.0;
+    for (int c = 0; c < c_ins; ++c) dot = dot + fq[a * c_ins + c] * f_ins[c];
+    const double sim = psm_sigmoid_t(dot, tab);
+    const double d0 = center[0] - mean[a * 3 + 0];
+    const double d1 = center[1] - mean[a * 3 + 1];
+    const double d2 = center[2] - mean[a * 3 + 2];
+    const double* m = inv + a * 9;
+    const double v0 = (m[0] * d0 + m[3] * d1) + m[6] * d2;
+    const double v1 = (m[1] * d0 + m[4] * d1) + m[7] * d2;
+    const double v2 = (m[2] * d0 + m[5] * d1) + m[8] * d2;
+    const double q = (d0 * v0 + d1 * v1) + d2 * v2;
+    const double geo = psm_exp_t(-0.5 * q, tab);
+    const double av = sim * geo;
+    a_vals[a * a_stride] = av;
+    a_max = av > a_max ? av : a_max;  // std::max(a_max, av)
+  }
+  double denom = 0;
+  for (int a = 0; a < n_alive; ++a) denom += psm_exp_t(a_vals[a * a_stride] - a_max, tab);
+  int best = 0;
+  double best_a = a_vals[0];
+  for (int a = 0; a < n_alive; ++a) {
+    const double av = a_vals[a * a_stride];
+    if (av > best_a) {
+      best = a;
+      best_a = av;
+    }
+    a_vals[a * a_stride] = psm_exp_t(av - a_max, tab) / denom;
+  }
+  return best;
+}
+
+#endif  // PSM_PANOPTIC_H
