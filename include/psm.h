@@ -178,6 +178,63 @@ int psm_render_batch(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam
 /* Counters of the most recent render, valid after psm_sync. */
 int psm_last_counters(const psm_ctx* ctx, psm_counters* out);
 
+/* ---- Panoptic layer ----------------------------
+ * A scene created with PSM_SCENE_EXACT_FEATURES also keeps fp64 copies of its
+ * features and labels on the device, so psm_render_panoptic reproduces the
+ * reference's fp64 feature/label sums (and hence its argmaxes) bit for bit. */
+#define PSM_SCENE_EXACT_FEATURES 1
+
+typedef struct psm_scene_desc {
+  const double* surfels13; /* N x 13 (Surfel: centre 3, quaternion w,x,y,z 4, scales 2, opacity, colour 3) */
+  int64_t n;
+  const double* f_sem;     /* N x C_sem row-major, may be NULL when c_sem == 0 */
+  int32_t c_sem;
+  const double* labels;    /* per-surfel N_q contiguous (MatX N_q x N column-major), may be NULL */
+  int32_t n_q;
+  const double* f_ins;     /* N x C_ins row-major (Surfel::f_ins; psm_assign_labels), may be NULL */
+  int32_t c_ins;
+  int32_t flags;           /* PSM_SCENE_EXACT_FEATURES */
+} psm_scene_desc;
+int psm_scene_create(psm_ctx* ctx, const psm_scene_desc* desc, psm_scene** out);
+
+/* Instance queries (InstanceQuery, core_types.hpp:76-84). `feature` holds the
+ * features assign_labels uses: InstanceQuery::feature, or the columns of its
+ * optional `features` matrix (panoptic.hpp:37). */
+typedef struct psm_queries {
+  int32_t n;
+  int32_t c_ins;
+  const double* feature;   /* n x c_ins */
+  const double* mean;      /* n x 3 */
+  const double* cov;       /* n x 9, column-major */
+  const int32_t* alive;    /* n */
+  const int32_t* class_id; /* n (used by psm_render_panoptic callers; may be NULL here) */
+} psm_queries;
+
+/* assign_labels (proj/src/panoptic.cpp:36-91) on the device. The scene's label
+ * channels become the N_q = queries->n column distribution (dead queries 0).
+ * dist_out (host, N x n, per-surfel contiguous) and argmax_out (host, N; -1 when
+ * no query is alive) may be NULL. The scene must have f_ins with c_ins ==
+ * queries->c_ins. Synchronous. */
+int psm_assign_labels(psm_ctx* ctx, psm_scene* scene, const psm_queries* queries, double* dist_out,
+                      int32_t* argmax_out);
+
+/* PanopticRender (metrics.hpp:70-78): int32 W*H planes, -1 = void. */
+typedef struct psm_panoptic_targets {
+  int32_t* ids;         /* label argmax where alpha_acc >= 0.5 */
+  int32_t* classes;     /* query_class[id] */
+  int32_t* sem_classes; /* first argmax of the semantic feature plane */
+  int32_t on_device;
+} psm_panoptic_targets;
+
+/* render_panoptic (proj/src/metrics.cpp:339-369) over a scene whose labels are
+ * assigned: the blend accumulates features and labels in fp64 in blend order and
+ * writes the three planes directly (no feature planes are materialised).
+ * query_class: n_query_class class ids (InstanceQuery::class_id). Needs a scene
+ * created with PSM_SCENE_EXACT_FEATURES. Same synchronisation rules as psm_render. */
+int psm_render_panoptic(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam,
+                        const psm_raster_config* cfg, const int32_t* query_class, int32_t n_query_class,
+                        const psm_panoptic_targets* targets, psm_counters* counters);
+
 /* Workload: make_street_scene (proj/src/synthetic.cpp:236-312) with the same
  * RNG draw order, plus `scale_mult` applied to s1 after it is drawn
  * (density-normalised variants; 1.0 = verbatim). Two-phase:
@@ -195,6 +252,8 @@ typedef struct psm_street_spec {
 } psm_street_spec;
 int psm_make_street_scene(const psm_street_spec* spec, int64_t* n_out, double* surfels13,
                           double* f_sem, double* labels, psm_camera* cam);
+/* The same scene's Surfel::f_ins (n x 8, 0.3 N(0,1) draws in the generator's order). */
+int psm_make_street_scene_ins(const psm_street_spec* spec, int64_t* n_out, double* f_ins);
 
 /* Camera::look_at / Camera::make (proj/src/core_types.cpp:18-60). */
 int psm_camera_look_at(const double eye[3], const double target[3], const double up[3], double fx,

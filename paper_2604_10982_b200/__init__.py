@@ -5,10 +5,12 @@ render_into / bench_render (proj/include/psimap/raster.hpp:142-172).
 """
 from .raster import (Binning, Blending, BenchReport, BenchRow, Camera, DeviceScene, PsmError, RasterConfig,
                      Renderer, RenderTargets, SceneMap, bench_render, render, render_into)
-from .scene import StreetSpec, density_scale, make_street_scene, trajectory_cameras
+from .scene import StreetSpec, density_scale, make_street_scene, street_f_ins, trajectory_cameras
+from .panoptic import InstanceQuery, PanopticRender, street_queries
 
 __all__ = [
     "Binning", "Blending", "BenchReport", "BenchRow", "Camera", "DeviceScene", "PsmError", "RasterConfig",
     "Renderer", "RenderTargets", "SceneMap", "bench_render", "render", "render_into", "StreetSpec",
-    "density_scale", "make_street_scene", "trajectory_cameras",
+    "density_scale", "make_street_scene", "trajectory_cameras", "street_f_ins", "InstanceQuery",
+    "PanopticRender", "street_queries",
 ]

@@ -60,9 +60,28 @@ class psm_street_spec(C.Structure):
                 ("image_h", C.c_int32), ("c_sem", C.c_int32), ("n_instances", C.c_int32), ("scale_mult", C.c_double)]
 
 
+PSM_SCENE_EXACT_FEATURES = 1
+
+
+class psm_scene_desc(C.Structure):
+    _fields_ = [("surfels13", C.c_void_p), ("n", C.c_int64), ("f_sem", C.c_void_p), ("c_sem", C.c_int32),
+                ("labels", C.c_void_p), ("n_q", C.c_int32), ("f_ins", C.c_void_p), ("c_ins", C.c_int32),
+                ("flags", C.c_int32)]
+
+
+class psm_queries(C.Structure):
+    _fields_ = [("n", C.c_int32), ("c_ins", C.c_int32), ("feature", C.c_void_p), ("mean", C.c_void_p),
+                ("cov", C.c_void_p), ("alive", C.c_void_p), ("class_id", C.c_void_p)]
+
+
+class psm_panoptic_targets(C.Structure):
+    _fields_ = [("ids", C.c_void_p), ("classes", C.c_void_p), ("sem_classes", C.c_void_p), ("on_device", C.c_int32)]
+
+
 # Every symbol include/psm.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED_SYMBOLS = (
     "psm_default_config", "psm_create", "psm_destroy", "psm_last_error", "psm_set_profiling", "psm_get_stage_times",
     "psm_sync", "psm_scene_upload", "psm_scene_free", "psm_scene_info", "psm_render", "psm_render_debug",
     "psm_render_batch", "psm_last_counters", "psm_make_street_scene", "psm_camera_look_at", "psm_camera_make",
+    "psm_scene_create", "psm_assign_labels", "psm_render_panoptic", "psm_make_street_scene_ins",
 )

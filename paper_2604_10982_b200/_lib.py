@@ -37,6 +37,11 @@ def load():
                                  P(A.psm_counters)]),
         "psm_render_debug": (C.c_int, [vp, vp, P(A.psm_camera), P(A.psm_raster_config), P(A.psm_targets),
                                        P(A.psm_counters), P(A.psm_debug)]),
+        "psm_scene_create": (C.c_int, [vp, P(A.psm_scene_desc), P(vp)]),
+        "psm_assign_labels": (C.c_int, [vp, vp, P(A.psm_queries), vp, vp]),
+        "psm_render_panoptic": (C.c_int, [vp, vp, P(A.psm_camera), P(A.psm_raster_config), vp, C.c_int32,
+                                          P(A.psm_panoptic_targets), P(A.psm_counters)]),
+        "psm_make_street_scene_ins": (C.c_int, [P(A.psm_street_spec), P(C.c_int64), vp]),
         "psm_render_batch": (C.c_int, [vp, vp, P(A.psm_camera), C.c_int32, P(A.psm_raster_config),
                                        P(A.psm_targets), P(A.psm_counters)]),
         "psm_last_counters": (C.c_int, [vp, P(A.psm_counters)]),

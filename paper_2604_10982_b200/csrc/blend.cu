@@ -162,7 +162,7 @@ __device__ __forceinline__ bool cull_meets(const SurfRec& r, float k, float x0, 
   return xl <= x1 && xr >= x0;
 }
 
-template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT>
+template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT, int PANO_T>
 __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(BlendParams p) {
   constexpr int kChunk = chunk_for(KMAX);
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -310,7 +310,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
           }
         }
         if constexpr (FULL_LIST) {
-          if (m < p.list_cap) p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(pos), __float_as_uint(wf));
+          if (m < p.list_cap) {
+            p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(pos), __float_as_uint(wf));
+            if constexpr (PANO_T > 0) p.lists_w[pix * p.list_cap + m] = wt;
+          }
         }
         T *= 1.0 - alpha;
         ++m;
@@ -484,11 +487,101 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
       }
     }
   }
+
+  // ---- panoptic planes (render_panoptic, metrics.cpp:339-369), fused: features and
+  // labels are accumulated in fp64 over the selected entries in blend order, exactly as
+  // raster.cpp:456-499 does (first entry writes, later ones add; --fmad=false), so the
+  // argmaxes are the reference's; only the three int planes are written.
+  if constexpr (PANO_T > 0) {
+    if constexpr (KMAX > 0) {  // selected entries back into blend (list position) order
+      for (int i = 1; i < blend_n; ++i) {
+        const int pi = top_p[i * kThreads + tid];
+        const double wi = top_w[i * kThreads + tid];
+        int j = i - 1;
+        while (j >= 0 && top_p[j * kThreads + tid] > pi) {
+          top_p[(j + 1) * kThreads + tid] = top_p[j * kThreads + tid];
+          top_w[(j + 1) * kThreads + tid] = top_w[j * kThreads + tid];
+          --j;
+        }
+        top_p[(j + 1) * kThreads + tid] = pi;
+        top_w[(j + 1) * kThreads + tid] = wi;
+      }
+    }
+    __syncwarp();
+    const int D = p.feat_dims, cs = p.c_sem;
+    const bool gate = inside && !(1.0 - T < 0.5);  // alpha_acc < 0.5 -> void (metrics.cpp:351)
+    int nsel = blend_n;
+    if constexpr (FULL_LIST) nsel = nsel < p.list_cap ? nsel : p.list_cap;
+    for (int q = 0; q < 32; ++q) {
+      const int qx = wx0 + (q & 7), qy = wy0 + (q >> 3);
+      const bool qgate = __shfl_sync(0xffffffffu, gate, q);
+      const int nq = __shfl_sync(0xffffffffu, nsel, q);
+      const int64_t qpix = static_cast<int64_t>(qy) * p.width + qx;
+      if (!qgate) {
+        if (lane == 0 && qx < p.width && qy < p.height) {
+          p.pan_ids[qpix] = -1;
+          p.pan_classes[qpix] = -1;
+          p.pan_sem[qpix] = -1;
+        }
+        continue;
+      }
+      double acc[PANO_T];
+#pragma unroll
+      for (int t = 0; t < PANO_T; ++t) acc[t] = 0.0;
+      for (int i = 0; i < (D > 0 ? nq : 0); ++i) {
+        int pos;
+        double w;
+        if constexpr (KMAX > 0) {
+          pos = top_p[i * kThreads + (tid & ~31) + q];
+          w = top_w[i * kThreads + (tid & ~31) + q];
+        } else {
+          pos = static_cast<int>(p.lists[qpix * p.list_cap + i].x);
+          w = p.lists_w[qpix * p.list_cap + i];
+        }
+        const double* row = p.feat64 + static_cast<int64_t>(__ldg(p.vals + pos)) * D;
+#pragma unroll
+        for (int t = 0; t < PANO_T; ++t) {
+          const int c = lane + 32 * t;
+          if (c < D) {
+            const double v = __ldg(row + c);
+            acc[t] = i == 0 ? w * v : acc[t] + w * v;
+          }
+        }
+      }
+      // first-max argmaxes over the semantic (c < cs) and label (c >= cs) channels
+      double bs = 0.0, bi = 0.0;
+      int ks = 0x7fffffff, ki = 0x7fffffff;
+#pragma unroll
+      for (int t = 0; t < PANO_T; ++t) {
+        const int c = lane + 32 * t;
+        if (c < cs) {
+          if (ks == 0x7fffffff || acc[t] > bs) { bs = acc[t]; ks = c; }
+        } else if (c < D) {
+          if (ki == 0x7fffffff || acc[t] > bi) { bi = acc[t]; ki = c - cs; }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, bs, o), oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int oks = __shfl_xor_sync(0xffffffffu, ks, o), oki = __shfl_xor_sync(0xffffffffu, ki, o);
+        if (oks != 0x7fffffff && (ks == 0x7fffffff || os > bs || (os == bs && oks < ks))) { bs = os; ks = oks; }
+        if (oki != 0x7fffffff && (ki == 0x7fffffff || oi > bi || (oi == bi && oki < ki))) { bi = oi; ki = oki; }
+      }
+      if (lane == 0) {
+        // ins_argmax stays -1 without labels or blends (raster.cpp:292,497); the
+        // semantic plane is all zeros when nothing blended, whose first max is 0
+        const int id = (p.n_q > 0 && nq > 0) ? ki : -1;
+        p.pan_ids[qpix] = id;
+        p.pan_classes[qpix] = (id >= 0 && id < p.n_query_class) ? __ldg(p.query_class + id) : -1;
+        p.pan_sem[qpix] = cs > 0 ? (nq > 0 ? ks : 0) : -1;
+      }
+    }
+  }
 }
 
-template <int KMAX, bool FULL, int VEC, int NV, int LPP, bool EXACT>
+template <int KMAX, bool FULL, int VEC, int NV, int LPP, bool EXACT, int PANO_T = 0>
 void launch_t(const BlendParams& p, int tiles, cudaStream_t st) {
-  auto kern = blend_kernel<KMAX, FULL, VEC, NV, LPP, EXACT>;
+  auto kern = blend_kernel<KMAX, FULL, VEC, NV, LPP, EXACT, PANO_T>;
   static unsigned long long configured = 0;  // per instantiation, one bit per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -520,6 +613,17 @@ void launch_feat(const BlendParams& p, int tiles, cudaStream_t st) {
   else launch_t<KMAX, FULL, 1, 16, 32, false>(p, tiles, st);
 }
 
+// Panoptic feature phase: PANO_T = channels per lane / 32 (feat_dims <= 32 * PANO_T).
+template <int KMAX, bool FULL>
+void launch_pano(const BlendParams& p, int tiles, cudaStream_t st) {
+  const int t = (p.feat_dims + 31) / 32;
+  if (t <= 1) launch_t<KMAX, FULL, 1, 0, 32, true, 1>(p, tiles, st);
+  else if (t <= 2) launch_t<KMAX, FULL, 1, 0, 32, true, 2>(p, tiles, st);
+  else if (t <= 4) launch_t<KMAX, FULL, 1, 0, 32, true, 4>(p, tiles, st);
+  else if (t <= 8) launch_t<KMAX, FULL, 1, 0, 32, true, 8>(p, tiles, st);
+  else launch_t<KMAX, FULL, 1, 0, 32, true, 16>(p, tiles, st);
+}
+
 }  // namespace
 
 #ifdef PSM_BLEND_STATS
@@ -547,6 +651,13 @@ int blend_nch_for(int feat_dims) {
 
 void launch_blend(const BlendParams& p, int tiles, bool topk, cudaStream_t st) {
   if (tiles <= 0) return;
+  if (p.pan_ids) {  // render_panoptic: fp64 blend-order feature phase and the three id planes
+    if (!topk) launch_pano<0, true>(p, tiles, st);
+    else if (blend_kmax_for(p.k_sel) == 8) launch_pano<8, false>(p, tiles, st);
+    else if (blend_kmax_for(p.k_sel) == 16) launch_pano<16, false>(p, tiles, st);
+    else launch_pano<32, false>(p, tiles, st);
+    return;
+  }
   if (!topk) {
     if (p.feat_dims == 0) launch_t<0, false, 1, 0, 32, true>(p, tiles, st);
     else launch_feat<0, true>(p, tiles, st);

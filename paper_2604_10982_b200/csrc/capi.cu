@@ -21,6 +21,7 @@
 
 #include "psm_device.cuh"
 #include "psm_kernels.h"
+#include "psm_panoptic.h"
 
 struct psm_scene {
   int device = 0;
@@ -28,6 +29,10 @@ struct psm_scene {
   int32_t c_sem = 0, n_q = 0;
   double* surfels = nullptr;  // N x 13 fp64
   float* feat = nullptr;      // N x (c_sem + n_q) fp32
+  double* feat64 = nullptr;   // N x (c_sem + n_q) fp64 (PSM_SCENE_EXACT_FEATURES)
+  double* f_ins = nullptr;    // N x c_ins fp64 (assign_labels)
+  int32_t c_ins = 0;
+  int32_t flags = 0;
 };
 
 namespace psm {
@@ -40,6 +45,10 @@ struct Buf {
 struct Planes {
   float *color, *depth, *normal, *sem, *ins, *alpha;
   int32_t *arg, *cnt;
+  // render_panoptic (pan_ids != NULL): the three id planes and the device query classes
+  int32_t *pan_ids = nullptr, *pan_classes = nullptr, *pan_sem = nullptr;
+  const int32_t* qclass = nullptr;
+  int32_t n_qclass = 0;
 };
 
 }  // namespace psm
@@ -62,6 +71,7 @@ struct psm_ctx {
   // scratch
   psm::Buf recs, bins, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, kscratch2, valid, pos, keys_c, src_c, keys_s, src_s;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
+  psm::Buf lists_w, pan_ids, pan_classes, pan_sem, qclass, lab_tmp;
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
   psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
@@ -295,6 +305,19 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->lists, npx * ctx->list_cap, &lists));
     bp.lists = lists;
     bp.list_cap = ctx->list_cap;
+    if (pl.pan_ids) {
+      double* lw;
+      PSM_TRY(ensure(ctx, ctx->lists_w, npx * ctx->list_cap, &lw));
+      bp.lists_w = lw;
+    }
+  }
+  if (pl.pan_ids) {
+    bp.feat64 = sc->feat64;
+    bp.pan_ids = pl.pan_ids;
+    bp.pan_classes = pl.pan_classes;
+    bp.pan_sem = pl.pan_sem;
+    bp.query_class = pl.qclass;
+    bp.n_query_class = pl.n_qclass;
   }
   if (!on_band) {
     launch_blend(bp, tiles, topk, st);
@@ -403,8 +426,13 @@ void read_times(psm_ctx* ctx) {
   cudaEventElapsedTime(&ctx->times.total, ctx->ev[0], ctx->ev[5]);
 }
 
+// pt != NULL: render_panoptic. The standard planes then live in context scratch, the
+// feature planes are not materialised, and pt's three id planes are the outputs.
 int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
-                  const psm_targets* tg, psm_counters* counters, psm_debug* dbg) {
+                  const psm_targets* tg_in, psm_counters* counters, psm_debug* dbg,
+                  const psm_panoptic_targets* pt = nullptr, const int32_t* qclass = nullptr, int32_t n_qclass = 0) {
+  const psm_targets scratch_only = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 1};
+  const psm_targets* tg = pt ? &scratch_only : tg_in;
   if (!ctx || !sc || !cam || !cfg || !tg) return fail(ctx, PSM_EINVAL, "null argument");
   if (cam->width <= 0 || cam->height <= 0) return fail(ctx, PSM_EINVAL, "camera: image size must be positive");
   PSM_TRY(check_config(ctx, cfg, sc->c_sem + sc->n_q));
@@ -431,9 +459,32 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
   PSM_TRY(pick(tg->blend_count, ctx->plane_cnt, npx, 4, reinterpret_cast<void**>(&pl.cnt)));
   pl.sem = nullptr;
   pl.ins = nullptr;
-  // feature planes are always produced (context scratch when the caller passes NULL)
-  if (cs > 0) PSM_TRY(pick(tg->sem_feat, ctx->plane_sem, npx * cs, 4, reinterpret_cast<void**>(&pl.sem)));
-  if (nq > 0) PSM_TRY(pick(tg->ins_dist, ctx->plane_ins, npx * nq, 4, reinterpret_cast<void**>(&pl.ins)));
+  // feature planes are always produced (context scratch when the caller passes NULL),
+  // except by render_panoptic, which reduces them to ids inside the blend
+  if (cs > 0 && !pt) PSM_TRY(pick(tg->sem_feat, ctx->plane_sem, npx * cs, 4, reinterpret_cast<void**>(&pl.sem)));
+  if (nq > 0 && !pt) PSM_TRY(pick(tg->ins_dist, ctx->plane_ins, npx * nq, 4, reinterpret_cast<void**>(&pl.ins)));
+  if (pt) {
+    if (!sc->feat64 && cs + nq > 0)
+      return fail(ctx, PSM_EUNSUPPORTED, "render_panoptic needs a scene created with PSM_SCENE_EXACT_FEATURES");
+    if (n_qclass < 0 || (n_qclass > 0 && !qclass)) return fail(ctx, PSM_EINVAL, "query classes");
+    auto pick_pan = [&](int32_t* user, psm::Buf& b, int32_t** out) -> int {
+      if (pt->on_device && user) {
+        *out = user;
+        return PSM_OK;
+      }
+      return ensure(ctx, b, npx, out);
+    };
+    PSM_TRY(pick_pan(pt->ids, ctx->pan_ids, &pl.pan_ids));
+    PSM_TRY(pick_pan(pt->classes, ctx->pan_classes, &pl.pan_classes));
+    PSM_TRY(pick_pan(pt->sem_classes, ctx->pan_sem, &pl.pan_sem));
+    int32_t* qc = nullptr;
+    PSM_TRY(ensure(ctx, ctx->qclass, static_cast<size_t>(n_qclass > 0 ? n_qclass : 1), &qc));
+    if (n_qclass > 0)
+      PSM_CUDA_TRY(cudaMemcpyAsync(qc, qclass, sizeof(int32_t) * n_qclass, cudaMemcpyHostToDevice, ctx->stream));
+    pl.qclass = qc;
+    pl.n_qclass = n_qclass;
+  }
+  const bool host_out = pt ? !pt->on_device : !tg->on_device;
   // host targets: each finished row band of every plane is copied on the copy stream while
   // the next band blends; the main stream then waits for the copies (the planes are
   // context scratch that the next frame overwrites)
@@ -456,15 +507,20 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
     PSM_TRY(d2h(tg->blend_count, pl.cnt, 1));
     if (pl.sem && tg->sem_feat) PSM_TRY(d2h(tg->sem_feat, pl.sem, cs));
     if (pl.ins && tg->ins_dist) PSM_TRY(d2h(tg->ins_dist, pl.ins, nq));
+    if (pt) {
+      PSM_TRY(d2h(pt->ids, pl.pan_ids, 1));
+      PSM_TRY(d2h(pt->classes, pl.pan_classes, 1));
+      PSM_TRY(d2h(pt->sem_classes, pl.pan_sem, 1));
+    }
     if (y1 == cam->height) {
       PSM_CUDA_TRY(cudaEventRecord(ctx->copy_done, cs_));
       PSM_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->copy_done, 0));
     }
     return PSM_OK;
   };
-  const BandHook* hook = tg->on_device ? nullptr : &band_d2h;
+  const BandHook* hook = host_out ? &band_d2h : nullptr;
   PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg, hook));
-  if (counters || !tg->on_device || ctx->profiling || dbg) {
+  if (counters || host_out || ctx->profiling || dbg) {
     for (int attempt = 0;; ++attempt) {
       PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
       bool rerun = false;
@@ -560,6 +616,7 @@ int psm_destroy(psm_ctx* ctx) {
                       &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s,
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
                       &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,
+                      &ctx->lists_w, &ctx->pan_ids, &ctx->pan_classes, &ctx->pan_sem, &ctx->qclass, &ctx->lab_tmp,
                       &ctx->plane_color, &ctx->plane_depth, &ctx->plane_normal, &ctx->plane_sem, &ctx->plane_ins,
                       &ctx->plane_arg, &ctx->plane_alpha, &ctx->plane_cnt};
   for (psm::Buf* b : bufs) psm::free_buf(*b);
@@ -601,14 +658,16 @@ int psm_last_counters(const psm_ctx* ctx, psm_counters* out) {
   return PSM_OK;
 }
 
-int psm_scene_upload(psm_ctx* ctx, const double* surfels13, int64_t n, const double* f_sem, int32_t c_sem,
-                     const double* labels, int32_t n_q, psm_scene** out) {
-  if (!ctx || !out) return PSM_EINVAL;
+int psm_scene_create(psm_ctx* ctx, const psm_scene_desc* d, psm_scene** out) {
+  if (!ctx || !out || !d) return PSM_EINVAL;
   *out = nullptr;
-  if (n < 0 || n > 0x7fffffffLL || c_sem < 0 || n_q < 0) return fail(ctx, PSM_EINVAL, "scene: bad sizes");
-  if (n > 0 && !surfels13) return fail(ctx, PSM_EINVAL, "scene: null surfels");
-  if (c_sem > 0 && n > 0 && !f_sem) return fail(ctx, PSM_EINVAL, "scene: null f_sem with c_sem > 0");
-  if (!labels) n_q = 0;
+  int64_t n = d->n;
+  int32_t c_sem = d->c_sem, n_q = d->n_q, c_ins = d->c_ins;
+  if (n < 0 || n > 0x7fffffffLL || c_sem < 0 || n_q < 0 || c_ins < 0) return fail(ctx, PSM_EINVAL, "scene: bad sizes");
+  if (n > 0 && !d->surfels13) return fail(ctx, PSM_EINVAL, "scene: null surfels");
+  if (c_sem > 0 && n > 0 && !d->f_sem) return fail(ctx, PSM_EINVAL, "scene: null f_sem with c_sem > 0");
+  if (!d->labels) n_q = 0;
+  if (!d->f_ins) c_ins = 0;
   if (n == 0) c_sem = 0;  // SceneMap::c_sem() of an empty scene (core_types.hpp:108)
   PSM_CUDA_TRY(cudaSetDevice(ctx->device));
   psm_scene* sc = new psm_scene();
@@ -616,18 +675,39 @@ int psm_scene_upload(psm_ctx* ctx, const double* surfels13, int64_t n, const dou
   sc->n = n;
   sc->c_sem = c_sem;
   sc->n_q = n_q;
+  sc->c_ins = c_ins;
+  sc->flags = d->flags;
   const int D = c_sem + n_q;
+  const bool exact = (d->flags & PSM_SCENE_EXACT_FEATURES) != 0;
   if (n > 0) {
     cudaError_t e = cudaMalloc(&sc->surfels, sizeof(double) * 13 * n);
-    if (e == cudaSuccess) e = cudaMemcpy(sc->surfels, surfels13, sizeof(double) * 13 * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(sc->surfels, d->surfels13, sizeof(double) * 13 * n, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && D > 0) {
+      std::vector<double> f64(exact ? static_cast<size_t>(n) * D : 0);
       std::vector<float> f(static_cast<size_t>(n) * D);
       for (int64_t i = 0; i < n; ++i) {
-        for (int c = 0; c < c_sem; ++c) f[i * D + c] = static_cast<float>(f_sem[i * c_sem + c]);
-        for (int q = 0; q < n_q; ++q) f[i * D + c_sem + q] = static_cast<float>(labels[i * n_q + q]);
+        for (int c = 0; c < c_sem; ++c) {
+          const double v = d->f_sem[i * c_sem + c];
+          f[i * D + c] = static_cast<float>(v);
+          if (exact) f64[i * D + c] = v;
+        }
+        for (int q = 0; q < n_q; ++q) {
+          const double v = d->labels[i * n_q + q];
+          f[i * D + c_sem + q] = static_cast<float>(v);
+          if (exact) f64[i * D + c_sem + q] = v;
+        }
       }
       e = cudaMalloc(&sc->feat, sizeof(float) * f.size());
       if (e == cudaSuccess) e = cudaMemcpy(sc->feat, f.data(), sizeof(float) * f.size(), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess && exact) {
+        e = cudaMalloc(&sc->feat64, sizeof(double) * f64.size());
+        if (e == cudaSuccess)
+          e = cudaMemcpy(sc->feat64, f64.data(), sizeof(double) * f64.size(), cudaMemcpyHostToDevice);
+      }
+    }
+    if (e == cudaSuccess && c_ins > 0) {
+      e = cudaMalloc(&sc->f_ins, sizeof(double) * c_ins * n);
+      if (e == cudaSuccess) e = cudaMemcpy(sc->f_ins, d->f_ins, sizeof(double) * c_ins * n, cudaMemcpyHostToDevice);
     }
     if (e != cudaSuccess) {
       psm_scene_free(ctx, sc);
@@ -638,12 +718,136 @@ int psm_scene_upload(psm_ctx* ctx, const double* surfels13, int64_t n, const dou
   return PSM_OK;
 }
 
+int psm_scene_upload(psm_ctx* ctx, const double* surfels13, int64_t n, const double* f_sem, int32_t c_sem,
+                     const double* labels, int32_t n_q, psm_scene** out) {
+  psm_scene_desc d{surfels13, n, f_sem, c_sem, labels, n_q, nullptr, 0, 0};
+  return psm_scene_create(ctx, &d, out);
+}
+
+int psm_assign_labels(psm_ctx* ctx, psm_scene* sc, const psm_queries* qs, double* dist_out, int32_t* argmax_out) {
+  if (!ctx || !sc || !qs) return PSM_EINVAL;
+  const int32_t nq = qs->n;
+  if (nq < 0 || (nq > 0 && (!qs->feature || !qs->mean || !qs->cov || !qs->alive)))
+    return fail(ctx, PSM_EINVAL, "assign_labels: bad queries");
+  if (sc->n > 0 && qs->c_ins != sc->c_ins)
+    return fail(ctx, PSM_EINVAL, "feature_similarity: dimension mismatch");  // panoptic.cpp:12-14
+  if (sc->c_sem + nq > 512) return fail(ctx, PSM_EUNSUPPORTED, "GPU path supports C_sem + N_q <= 512");
+  PSM_CUDA_TRY(cudaSetDevice(ctx->device));
+  PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the scene's buffers may be in use by a render
+  const int64_t n = sc->n;
+  const int c_ins = qs->c_ins;
+  // alive queries and their inverse covariances (panoptic.cpp:44-62), host side, once
+  std::vector<int32_t> alive_index, alive_slot(static_cast<size_t>(nq > 0 ? nq : 1), -1);
+  for (int q = 0; q < nq; ++q)
+    if (qs->alive[q]) {
+      alive_slot[q] = static_cast<int32_t>(alive_index.size());
+      alive_index.push_back(q);
+    }
+  const int na = static_cast<int>(alive_index.size());
+  std::vector<double> qtab(static_cast<size_t>(na) * (c_ins + 12) + 1);
+  double* fq = qtab.data();
+  double* mean = fq + static_cast<size_t>(na) * c_ins;
+  double* inv = mean + 3 * na;
+  for (int a = 0; a < na; ++a) {
+    const int q = alive_index[a];
+    for (int c = 0; c < c_ins; ++c) fq[a * c_ins + c] = qs->feature[static_cast<int64_t>(q) * c_ins + c];
+    for (int i = 0; i < 3; ++i) mean[a * 3 + i] = qs->mean[q * 3 + i];
+    psm_query_inverse(qs->cov + q * 9, inv + a * 9);
+  }
+  const int D = sc->c_sem + nq;
+  const bool exact = sc->feat64 != nullptr || (sc->flags & PSM_SCENE_EXACT_FEATURES);
+  float* feat = nullptr;
+  double *feat64 = nullptr, *dqtab = nullptr, *scratch = nullptr, *ddist = nullptr;
+  int32_t *didx = nullptr, *darg = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(dqtab); cudaFree(scratch); cudaFree(ddist); cudaFree(didx); cudaFree(darg);
+  };
+  cudaError_t e = cudaSuccess;
+  if (n > 0 && D > 0) e = cudaMalloc(&feat, sizeof(float) * n * D);
+  if (e == cudaSuccess && n > 0 && D > 0 && exact) e = cudaMalloc(&feat64, sizeof(double) * n * D);
+  if (e == cudaSuccess) e = cudaMalloc(&dqtab, sizeof(double) * qtab.size());
+  if (e == cudaSuccess) e = cudaMemcpy(dqtab, qtab.data(), sizeof(double) * qtab.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&didx, sizeof(int32_t) * (na + (nq > 0 ? nq : 1)));
+  if (e == cudaSuccess && na > 0)
+    e = cudaMemcpy(didx, alive_index.data(), sizeof(int32_t) * na, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(didx + na, alive_slot.data(), sizeof(int32_t) * (nq > 0 ? nq : 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && n > 0 && na > 0) e = cudaMalloc(&scratch, sizeof(double) * n * na);
+  if (e == cudaSuccess && n > 0 && dist_out && nq > 0) e = cudaMalloc(&ddist, sizeof(double) * n * nq);
+  if (e == cudaSuccess && n > 0 && argmax_out) e = cudaMalloc(&darg, sizeof(int32_t) * n);
+  if (e != cudaSuccess) {
+    cleanup();
+    cudaFree(feat);
+    cudaFree(feat64);
+    return psm::fail_cuda(ctx, e, "assign_labels buffers", __FILE__, __LINE__);
+  }
+  psm::LabelParams lp;
+  lp.n = n;
+  lp.c_sem = sc->c_sem;
+  lp.n_q = nq;
+  lp.d_in = sc->c_sem + sc->n_q;
+  lp.c_ins = c_ins;
+  lp.n_alive = na;
+  lp.surfels = sc->surfels;
+  lp.f_ins = sc->f_ins;
+  lp.feat_in = sc->feat;
+  lp.feat64_in = sc->feat64;
+  lp.feat_out = feat;
+  lp.feat64_out = feat64;
+  lp.q_feat = dqtab;
+  lp.q_mean = dqtab + static_cast<size_t>(na) * c_ins;
+  lp.q_inv = lp.q_mean + 3 * na;
+  lp.alive_index = didx;
+  lp.alive_slot = didx + na;
+  lp.scratch = scratch;
+  lp.dist = ddist;
+  lp.argmax = darg;
+  if (n > 0 && (D > 0 || argmax_out)) {
+    if (c_ins > 0 && !sc->f_ins) {
+      cleanup();
+      cudaFree(feat);
+      cudaFree(feat64);
+      return fail(ctx, PSM_EINVAL, "assign_labels: the scene has no f_ins");
+    }
+    if (D > 0 || darg) psm::launch_assign_labels(lp, ctx->stream);
+  }
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess && ddist) e = cudaMemcpy(dist_out, ddist, sizeof(double) * n * nq, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && darg) e = cudaMemcpy(argmax_out, darg, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && argmax_out && n > 0 && na == 0)
+    for (int64_t i = 0; i < n; ++i) argmax_out[i] = -1;
+  cleanup();
+  if (e != cudaSuccess) {
+    cudaFree(feat);
+    cudaFree(feat64);
+    return psm::fail_cuda(ctx, e, "assign_labels", __FILE__, __LINE__);
+  }
+  if (n > 0 && D > 0) {
+    cudaFree(sc->feat);
+    cudaFree(sc->feat64);
+    sc->feat = feat;
+    sc->feat64 = feat64;
+  }
+  sc->n_q = nq;
+  return PSM_OK;
+}
+
+int psm_render_panoptic(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam, const psm_raster_config* cfg,
+                        const int32_t* query_class, int32_t n_query_class, const psm_panoptic_targets* targets,
+                        psm_counters* counters) {
+  if (!targets) return PSM_EINVAL;
+  return psm::render_common(ctx, scene, cam, cfg, nullptr, counters, nullptr, targets, query_class, n_query_class);
+}
+
 int psm_scene_free(psm_ctx* ctx, psm_scene* sc) {
   (void)ctx;
   if (!sc) return PSM_OK;
   cudaSetDevice(sc->device);
   if (sc->surfels) cudaFree(sc->surfels);
   if (sc->feat) cudaFree(sc->feat);
+  if (sc->feat64) cudaFree(sc->feat64);
+  if (sc->f_ins) cudaFree(sc->f_ins);
   delete sc;
   return PSM_OK;
 }

@@ -161,8 +161,8 @@ int psm_camera_look_at(const double eye_[3], const double target_[3], const doub
   return psm_camera_make(r_cw, t, fx, fy, 0.5 * width, 0.5 * height, width, height, near_clip, far_clip, out);
 }
 
-int psm_make_street_scene(const psm_street_spec* spec, int64_t* n_out, double* surfels13, double* f_sem,
-                          double* labels, psm_camera* cam) {
+static int street_scene(const psm_street_spec* spec, int64_t* n_out, double* surfels13, double* f_sem,
+                        double* labels, double* f_ins, psm_camera* cam) {
   if (!spec || !n_out) return PSM_EINVAL;
   if (spec->n_surfels < 0 || spec->c_sem < 0 || spec->n_instances < 1) return PSM_EINVAL;
   struct Group {
@@ -232,7 +232,10 @@ int psm_make_street_scene(const psm_street_spec* spec, int64_t* n_out, double* s
         const double v = rng.normal();
         if (f_sem) f_sem[at * spec->c_sem + c] = v;
       }
-      for (int c = 0; c < c_ins; ++c) (void)(0.3 * rng.normal());  // f_ins: unused by render, drawn for RNG order
+      for (int c = 0; c < c_ins; ++c) {  // f_ins: unused by render (drawn for the RNG order); assign_labels
+        const double v = 0.3 * rng.normal();
+        if (f_ins) f_ins[at * c_ins + c] = v;
+      }
     }
   }
   if (labels) {  // near one-hot per structural instance (synthetic.cpp:298-309)
@@ -246,6 +249,21 @@ int psm_make_street_scene(const psm_street_spec* spec, int64_t* n_out, double* s
     }
   }
   return PSM_OK;
+}
+
+int psm_make_street_scene(const psm_street_spec* spec, int64_t* n_out, double* surfels13, double* f_sem,
+                          double* labels, psm_camera* cam) {
+  return street_scene(spec, n_out, surfels13, f_sem, labels, nullptr, cam);
+}
+
+int psm_make_street_scene_ins(const psm_street_spec* spec, int64_t* n_out, double* f_ins) {
+  int64_t n = 0;
+  int st = street_scene(spec, &n, nullptr, nullptr, nullptr, nullptr, nullptr);
+  if (st != PSM_OK) return st;
+  if (n_out) *n_out = n;
+  if (!f_ins) return PSM_OK;
+  std::vector<double> tmp(static_cast<size_t>(n > 0 ? n : 1) * 13);
+  return street_scene(spec, &n, tmp.data(), nullptr, nullptr, f_ins, nullptr);
 }
 
 }  // extern "C"

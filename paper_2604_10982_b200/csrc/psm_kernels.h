@@ -27,7 +27,33 @@ struct BlendParams {
   uint2* lists;           // full blending with features: [W*H][list_cap]
   int32_t list_cap;
   int32_t* list_overflow;
+  // panoptic epilogue (render_panoptic, metrics.cpp:339-369): when pan_ids != NULL the
+  // feature phase accumulates feat64 in fp64 in blend order and writes these planes
+  const double* feat64;   // [N][feat_dims] fp64
+  double* lists_w;        // full blending: fp64 weights beside `lists`
+  int32_t *pan_ids, *pan_classes, *pan_sem;
+  const int32_t* query_class;
+  int32_t n_query_class;
 };
+
+// assign_labels (panoptic.cpp:36-91), labels.cu
+struct LabelParams {
+  int64_t n;
+  int32_t c_sem, n_q, d_in, c_ins, n_alive;
+  const double* surfels;     // [N][13]
+  const double* f_ins;       // [N][c_ins]
+  const float* feat_in;      // old rows [N][d_in] (f_sem columns first)
+  const double* feat64_in;   // may be NULL
+  float* feat_out;           // new rows [N][c_sem + n_q]
+  double* feat64_out;        // may be NULL
+  const double *q_feat, *q_mean, *q_inv;  // alive queries: [a][c_ins], [a][3], [a][9] column-major
+  const int32_t* alive_index;  // alive slot -> query
+  const int32_t* alive_slot;   // query -> alive slot or -1
+  double* scratch;           // [n_alive][N]
+  double* dist;              // optional [N][n_q]
+  int32_t* argmax;           // optional [N]
+};
+void launch_assign_labels(const LabelParams& p, cudaStream_t st);
 
 // K1 preprocess.cu
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,

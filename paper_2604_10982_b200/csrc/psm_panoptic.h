@@ -94,7 +94,7 @@ PSM_PHD void psm_query_inverse(const double* cov, double* inv) {
 // inv[a * 9 + c * 3 + r] (column-major). Writes A to a_vals[a * a_stride] and then the
 // softmax probability over it (in place); returns the argmax among the alive queries.
 PSM_PHD int psm_assign_one(const double* f_ins, int c_ins, const double* center, int n_alive, const double* fq,
-                           const double* mean, const double* inv, double* a_vals, int a_stride,
+                           const double* mean, const double* inv, double* a_vals, int64_t a_stride,
                            const uint64_t* tab) {
   double a_max = -1;
   for (int a = 0; a < n_alive; ++a) {

@@ -16,7 +16,7 @@ import ctypes as C
 import enum
 import math
 from dataclasses import dataclass, field
-from typing import List, Optional
+from typing import Tuple, List, Optional
 
 import numpy as np
 
@@ -146,13 +146,17 @@ class SceneMap:
     surfels as an (N, 13) fp64 array [center3, quat(w,x,y,z)4, scales2, opacity, color3]
     (Surfel, core_types.hpp:17-25) and f_sem as (N, C_sem) fp64."""
 
-    def __init__(self, surfels13: np.ndarray, f_sem: Optional[np.ndarray] = None):
+    def __init__(self, surfels13: np.ndarray, f_sem: Optional[np.ndarray] = None,
+                 f_ins: Optional[np.ndarray] = None, queries=None):
         self.surfels = np.ascontiguousarray(np.asarray(surfels13, dtype=np.float64).reshape(-1, 13))
         n = self.surfels.shape[0]
         f = np.zeros((n, 0)) if f_sem is None else np.asarray(f_sem, dtype=np.float64)
         if n == 0:
             f = f.reshape(0, f.shape[-1] if f.ndim == 2 else 0)
         self.f_sem = np.ascontiguousarray(f.reshape(n, -1) if n else f)
+        # Surfel::f_ins (N, C_ins) and SceneMap::queries (core_types.hpp:105): the panoptic layer's inputs
+        self.f_ins = None if f_ins is None else np.ascontiguousarray(np.asarray(f_ins, dtype=np.float64).reshape(n, -1))
+        self.queries = list(queries) if queries is not None else []
 
     def __len__(self) -> int:
         return self.surfels.shape[0]
@@ -199,7 +203,7 @@ def _ptr(a: Optional[np.ndarray]):
 class DeviceScene:
     """A scene resident on one GPU (psm_scene_upload)."""
 
-    def __init__(self, renderer: "Renderer", scene: SceneMap, labels: Optional[np.ndarray]):
+    def __init__(self, renderer: "Renderer", scene: SceneMap, labels: Optional[np.ndarray], exact: bool = False):
         self._r = renderer
         lib = _lib.load()
         n = len(scene)
@@ -212,9 +216,14 @@ class DeviceScene:
                 raise ValueError("labels must be (N, N_q): one distribution per surfel")
             n_q = lab.shape[1]
         self.handle = C.c_void_p()
-        _check(lib.psm_scene_upload(renderer.ctx, _ptr(scene.surfels), n, _ptr(scene.f_sem), scene.c_sem(),
-                                    _ptr(lab), n_q, C.byref(self.handle)), renderer.ctx, "scene upload")
+        f_ins = getattr(scene, "f_ins", None)
+        c_ins = 0 if f_ins is None else f_ins.shape[1]
+        desc = A.psm_scene_desc(_ptr(scene.surfels), n, _ptr(scene.f_sem), scene.c_sem(), _ptr(lab), n_q,
+                                _ptr(f_ins), c_ins, A.PSM_SCENE_EXACT_FEATURES if exact else 0)
+        _check(lib.psm_scene_create(renderer.ctx, C.byref(desc), C.byref(self.handle)), renderer.ctx, "scene upload")
         self.n, self.c_sem, self.n_q = n, (scene.c_sem() if n else 0), (n_q if lab is not None else 0)
+        self.c_ins = c_ins
+        self.exact = exact
 
     def free(self) -> None:
         if self.handle:
@@ -250,8 +259,52 @@ class Renderer:
         except Exception:
             pass
 
-    def upload(self, scene: SceneMap, labels: Optional[np.ndarray] = None) -> DeviceScene:
-        return DeviceScene(self, scene, labels)
+    def upload(self, scene: SceneMap, labels: Optional[np.ndarray] = None, exact: bool = False) -> DeviceScene:
+        """psm_scene_create. exact=True also keeps fp64 features/labels on the device
+        (render_panoptic reproduces the reference's argmaxes bit for bit)."""
+        return DeviceScene(self, scene, labels, exact)
+
+    def assign_labels(self, dscene: DeviceScene, queries) -> Tuple[np.ndarray, np.ndarray]:
+        """assign_labels (panoptic.cpp:36-91) on the GPU: the scene's label channels become
+        the per-surfel distribution over `queries`. Returns (dist (N, Q), argmax (N,))."""
+        from .panoptic import pack_queries
+        lib = _lib.load()
+        feat, mean, cov, alive, cls = pack_queries(queries, dscene.c_ins)
+        q = len(queries)
+        qs = A.psm_queries(q, dscene.c_ins, _ptr(feat), _ptr(mean), _ptr(cov), _ptr(alive), _ptr(cls))
+        dist = np.zeros((dscene.n, q))
+        arg = np.full(dscene.n, -1, np.int32)
+        _check(lib.psm_assign_labels(self.ctx, dscene.handle, C.byref(qs), _ptr(dist), _ptr(arg)), self.ctx,
+               "assign_labels")
+        dscene.n_q = q
+        return dist, arg
+
+    def render_panoptic(self, dscene: DeviceScene, cam: Camera, cfg: RasterConfig, query_class,
+                        counters: bool = False):
+        """render_panoptic (metrics.cpp:339-369) over a DeviceScene whose labels are assigned
+        (assign_labels or uploaded): PanopticRender of (H, W, 1) int32 planes."""
+        from .panoptic import PanopticRender
+        lib = _lib.load()
+        h, w = cam.height, cam.width
+        ids = np.empty((h, w, 1), np.int32)
+        classes = np.empty((h, w, 1), np.int32)
+        sem = np.empty((h, w, 1), np.int32)
+        qc = np.ascontiguousarray(np.asarray(list(query_class), dtype=np.int32))
+        pt = A.psm_panoptic_targets(_ptr(ids), _ptr(classes), _ptr(sem), 0)
+        cnt = A.psm_counters()
+        c_cam, c_cfg = cam.to_c(), cfg.to_c()
+        _check(lib.psm_render_panoptic(self.ctx, dscene.handle, C.byref(c_cam), C.byref(c_cfg), _ptr(qc), qc.size,
+                                       C.byref(pt), C.byref(cnt)), self.ctx, "render_panoptic")
+        out = PanopticRender(ids, classes, sem)
+        return (out, cnt) if counters else out
+
+    def render_panoptic_scene(self, scene: SceneMap, cam: Camera, cfg: RasterConfig):
+        """psimap::render_panoptic(scene, cam, cfg): assign_labels over scene.queries, render,
+        epilogue, all on the GPU."""
+        ds = DeviceScene(self, scene, None, exact=True)
+        if scene.queries:
+            self.assign_labels(ds, scene.queries)
+        return self.render_panoptic(ds, cam, cfg, [q.class_id for q in scene.queries])
 
     def set_profiling(self, on: bool) -> None:
         _lib.load().psm_set_profiling(self.ctx, int(on))

@@ -53,6 +53,18 @@ def make_street_scene(spec: StreetSpec, with_labels: bool = True) -> Tuple[Scene
     return SceneMap(surfels, f_sem), labels, Camera.from_c(cam)
 
 
+def street_f_ins(spec: StreetSpec) -> np.ndarray:
+    """Surfel::f_ins of make_street_scene (N, 8): the 0.3 N(0,1) draws the generator makes
+    for every surfel (synthetic.cpp:283-284), for assign_labels."""
+    lib = _lib.load()
+    cs = spec.to_c()
+    n = C.c_int64()
+    _check(lib.psm_make_street_scene_ins(C.byref(cs), C.byref(n), None), what="street f_ins")
+    f = np.empty((n.value, 8), dtype=np.float64)
+    _check(lib.psm_make_street_scene_ins(C.byref(cs), C.byref(n), f.ctypes.data_as(C.c_void_p)), what="street f_ins")
+    return f
+
+
 def trajectory_cameras(n_views: int, width: int, height: int, first: int = 0, count: Optional[int] = None,
                        total: int = 256) -> List[Camera]:
     """C5 views i in [first, first+count) of a closed-form `total`-view trajectory:
