@@ -26,6 +26,8 @@ WORKLOADS = {
     "c1": (10_000, 256, 256, 0, "full", 16, "10k surfels 256x256 RGB+depth"),
     "c2": (1_000_000, 1280, 720, 0, "full", 16, "1M surfels 1280x720 RGB+depth+normal"),
     "c3": (1_000_000, 1280, 720, 64, "topk", 8, "1M surfels 1280x720 64-d semantics Top-K=8"),
+    "c3p": (1_000_000, 1280, 720, 64, "topk", 8, "render_panoptic over 1M surfels 1280x720 64-d semantics, "
+                                                 "32 instance queries (assign_labels each frame), Top-K=8"),
     "c4": (5_000_000, 1920, 1080, 128, "topk", 16, "5M surfels 1920x1080 128-d semantics Top-K=16"),
     "c5": (5_000_000, 1920, 1080, 128, "topk", 16, "256-view trajectory over 5M surfels 1920x1080 128-d Top-K=16, "
                                                      "views sharded across ranks"),
@@ -99,12 +101,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+C3P_QUERIES = 32
+
+
 def build_workload(name, rank, world):
-    from paper_2604_10982_b200 import StreetSpec, density_scale, make_street_scene, trajectory_cameras
+    from paper_2604_10982_b200 import (SceneMap, StreetSpec, density_scale, make_street_scene, street_f_ins,
+                                       street_queries, trajectory_cameras)
     n, w, h, c, blending, k, desc = WORKLOADS[name]
     t0 = time.perf_counter()
-    scene, _, cam0 = make_street_scene(StreetSpec(n_surfels=n, image_w=w, image_h=h, c_sem=c,
-                                                  scale_mult=density_scale(n, w, h)), with_labels=False)
+    spec = StreetSpec(n_surfels=n, image_w=w, image_h=h, c_sem=c, scale_mult=density_scale(n, w, h))
+    scene, _, cam0 = make_street_scene(spec, with_labels=False)
+    if name == "c3p":  # the panoptic layer's inputs: Surfel::f_ins and synthetic instance queries
+        scene = SceneMap(scene.surfels, scene.f_sem, street_f_ins(spec), street_queries(C3P_QUERIES))
     if name == "c5":
         # the rank's contiguous block of the closed-form 256-view trajectory
         from paper_2604_10982_b200.multiview import shard_range
@@ -132,7 +140,10 @@ def cpu_reference(scene, cam, cfg, frames):
     times = []
     for _ in range(frames):
         t0 = time.perf_counter()
-        O.render(scene, None, cam, cfg, planes=False, libm=True)
+        if scene.queries:  # render_panoptic (metrics.cpp:339-369): assign_labels + render + epilogue
+            O.render_panoptic(scene, scene.f_ins, scene.queries, cam, cfg)
+        else:
+            O.render(scene, None, cam, cfg, planes=False, libm=True)
         times.append(time.perf_counter() - t0)
     threads = int(os.environ.get("PSIMAP_THREADS", 0)) or os.cpu_count()
     return 1.0 / min(times), threads, times
@@ -182,8 +193,12 @@ def run_ours(args):
     cfg = raster_cfg(blending, k)
     stream = torch.cuda.Stream(device=dev)
     r = Renderer(local_rank, stream=stream.cuda_stream)
+    pano = bool(scene.queries)  # c3p: render_panoptic (assign_labels + fused panoptic blend) per frame
     t0 = time.perf_counter()
-    ds = r.upload(scene)
+    ds = r.upload(scene, exact=pano)
+    qclass = np.array([q.class_id for q in scene.queries], np.int32)
+    if pano:
+        r.assign_labels(ds, scene.queries)
     torch.cuda.synchronize()
     upload_s = time.perf_counter() - t0
     npx = w * h
@@ -196,14 +211,22 @@ def run_ours(args):
         "alpha_acc": torch.empty(npx, dtype=torch.float32, device=dev),
         "blend_count": torch.empty(npx, dtype=torch.int32, device=dev),
     }
+    if pano:
+        planes_t = {kk: torch.empty(npx, dtype=torch.int32, device=dev) for kk in ("ids", "classes", "sem_classes")}
     ptrs = {kk: v.data_ptr() for kk, v in planes_t.items()}
+
+    def frame(cv, counters):
+        if pano:  # psimap::render_panoptic: assign_labels, then the render with the fused epilogue
+            r.assign_labels(ds, scene.queries, outputs=False)
+            return r.render_panoptic_device(ds, cv, cfg, qclass, ptrs, counters=counters)
+        return r.render_device(ds, cv, cfg, ptrs, counters=counters)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
     # warm-up (also sizes every grow-only buffer)
     r.set_profiling(True)
     cnt = None
     for _ in range(max(args.warmup, 1)):
-        cnt = r.render_device(ds, cam, cfg, ptrs, counters=True)
+        cnt = frame(cam, True)
     n_proj = int(cnt.n_proj)
 
     # timed region: per step, flush L2 (outside the events), then one render between events on its stream
@@ -218,7 +241,7 @@ def run_ours(args):
                 flush.zero_()
                 ev[i][0].record(stream)
             for cv in cams:
-                r.render_device(ds, cv, cfg, ptrs, counters=False)
+                frame(cv, False)
                 if len(cams) > 1:
                     r.sync()
                     st = r.stage_times()
@@ -240,10 +263,38 @@ def run_ours(args):
         total_ms = float(t.item())
     r.set_profiling(False)
     cnt = r.sync()
+    assign_ms = None
+    if pano:  # assign_labels alone, device-timed on the render stream
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        for _ in range(5):
+            r.assign_labels(ds, scene.queries, outputs=False)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        torch.cuda.synchronize()
+        assign_ms = e0.elapsed_time(e1) / 5
 
     # e2e through the C-ABI with host (pinned) targets: D2H of every plane inside each step
     e2e = None
-    if rank == 0 or world > 1:
+    if pano:
+        from paper_2604_10982_b200.panoptic import PanopticRender
+        pr = PanopticRender(*(torch.empty((h, w, 1), dtype=torch.int32, pin_memory=True).numpy() for _ in range(3)))
+        r.render_panoptic(ds, cam, cfg, qclass, out=pr)  # warm
+        torch.cuda.synchronize()
+        e2e_steps = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            r.assign_labels(ds, scene.queries, outputs=False)
+            r.render_panoptic(ds, cam, cfg, qclass, out=pr)
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        e2e = {"value": 1.0 / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": C.sizeof(A.psm_camera),
+               "d2h_bytes_per_step": int(pr.ids.nbytes + pr.classes.nbytes + pr.sem_classes.nbytes),
+               "steps": e2e_steps,
+               "note": "assign_labels (async) + psm_render_panoptic with host targets: the three int32 id planes "
+                       "copied back per frame to pinned memory; scene resident (exact fp64 features, upload "
+                       f"{upload_s * 1000:.0f} ms once)"}
+    elif rank == 0 or world > 1:
         from paper_2604_10982_b200.raster import RenderTargets
         host = RenderTargets()
         host.ensure(w, h, c, 0)
@@ -280,6 +331,10 @@ def run_ours(args):
     frames = args.steps * views_total
     value = frames / (total_ms / 1000.0)
     b_frame, b_blend = alg_bytes(n, n_proj, w, h, c)
+    if pano:  # fp64 feature + label rows read; 44 B/px of planes plus 12 B/px of ids written
+        d = c + len(scene.queries)
+        b_blend = 8 * d * n_proj + w * h * 56
+        b_frame = 52 * n + 64 * n + 12 * len(scene.queries) * n + b_blend
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -311,6 +366,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: {desc}", "binning": "ellipse (precise tile intersection)",
+                   "queries": len(scene.queries), "assign_labels_ms": assign_ms,
                    "blending": blending, "top_k": k, "surfels": n, "n_proj": n_proj, "width": w, "height": h,
                    "c_sem": c, "rn_total": int(cnt.rn_total), "blended_total": int(cnt.blended_total),
                    "l2": "flushed between timed steps (256 MB write outside the events)",
@@ -322,9 +378,10 @@ def run_ours(args):
                      "peak_source": peak_src, "alg_bytes_per_launch": b_blend, "launch_ms": blend_avg},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 8 * args.steps,
+        "gpu_launches": (9 if pano else 8) * args.steps,
         "gpu_launches_note": "per step: preprocess, tile_sub_scan, tile_scan, emit, sort_tiles<1024>, "
-                             "sort_tiles_huge, sort_tiles<128>, blend (+3 memsets, 1 small H2D)",
+                             "sort_tiles_huge, sort_tiles<128>, blend (+3 memsets, 1 small H2D)"
+                             + ("; c3p adds assign_labels" if pano else ""),
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -71,7 +71,7 @@ struct psm_ctx {
   // scratch
   psm::Buf recs, bins, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, kscratch2, valid, pos, keys_c, src_c, keys_s, src_s;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
-  psm::Buf lists_w, pan_ids, pan_classes, pan_sem, qclass, lab_tmp;
+  psm::Buf lists_w, pan_ids, pan_classes, pan_sem, qclass, lab_tmp, lab_scratch, lab_dist, lab_arg;
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
   psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
@@ -617,6 +617,7 @@ int psm_destroy(psm_ctx* ctx) {
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
                       &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,
                       &ctx->lists_w, &ctx->pan_ids, &ctx->pan_classes, &ctx->pan_sem, &ctx->qclass, &ctx->lab_tmp,
+                      &ctx->lab_scratch, &ctx->lab_dist, &ctx->lab_arg,
                       &ctx->plane_color, &ctx->plane_depth, &ctx->plane_normal, &ctx->plane_sem, &ctx->plane_ins,
                       &ctx->plane_arg, &ctx->plane_alpha, &ctx->plane_cnt};
   for (psm::Buf* b : bufs) psm::free_buf(*b);
@@ -733,7 +734,6 @@ int psm_assign_labels(psm_ctx* ctx, psm_scene* sc, const psm_queries* qs, double
     return fail(ctx, PSM_EINVAL, "feature_similarity: dimension mismatch");  // panoptic.cpp:12-14
   if (sc->c_sem + nq > 512) return fail(ctx, PSM_EUNSUPPORTED, "GPU path supports C_sem + N_q <= 512");
   PSM_CUDA_TRY(cudaSetDevice(ctx->device));
-  PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the scene's buffers may be in use by a render
   const int64_t n = sc->n;
   const int c_ins = qs->c_ins;
   // alive queries and their inverse covariances (panoptic.cpp:44-62), host side, once
@@ -756,31 +756,32 @@ int psm_assign_labels(psm_ctx* ctx, psm_scene* sc, const psm_queries* qs, double
   }
   const int D = sc->c_sem + nq;
   const bool exact = sc->feat64 != nullptr || (sc->flags & PSM_SCENE_EXACT_FEATURES);
-  float* feat = nullptr;
-  double *feat64 = nullptr, *dqtab = nullptr, *scratch = nullptr, *ddist = nullptr;
-  int32_t *didx = nullptr, *darg = nullptr;
-  auto cleanup = [&]() {
-    cudaFree(dqtab); cudaFree(scratch); cudaFree(ddist); cudaFree(didx); cudaFree(darg);
-  };
-  cudaError_t e = cudaSuccess;
-  if (n > 0 && D > 0) e = cudaMalloc(&feat, sizeof(float) * n * D);
-  if (e == cudaSuccess && n > 0 && D > 0 && exact) e = cudaMalloc(&feat64, sizeof(double) * n * D);
-  if (e == cudaSuccess) e = cudaMalloc(&dqtab, sizeof(double) * qtab.size());
-  if (e == cudaSuccess) e = cudaMemcpy(dqtab, qtab.data(), sizeof(double) * qtab.size(), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMalloc(&didx, sizeof(int32_t) * (na + (nq > 0 ? nq : 1)));
-  if (e == cudaSuccess && na > 0)
-    e = cudaMemcpy(didx, alive_index.data(), sizeof(int32_t) * na, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess)
-    e = cudaMemcpy(didx + na, alive_slot.data(), sizeof(int32_t) * (nq > 0 ? nq : 1), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && n > 0 && na > 0) e = cudaMalloc(&scratch, sizeof(double) * n * na);
-  if (e == cudaSuccess && n > 0 && dist_out && nq > 0) e = cudaMalloc(&ddist, sizeof(double) * n * nq);
-  if (e == cudaSuccess && n > 0 && argmax_out) e = cudaMalloc(&darg, sizeof(int32_t) * n);
-  if (e != cudaSuccess) {
-    cleanup();
-    cudaFree(feat);
-    cudaFree(feat64);
-    return psm::fail_cuda(ctx, e, "assign_labels buffers", __FILE__, __LINE__);
+  cudaStream_t st = ctx->stream;
+  // the rows are rewritten in place when the width is unchanged (each thread reads its
+  // own row's f_sem columns before writing it); otherwise into new buffers
+  const bool in_place = nq == sc->n_q && (D == 0 || (sc->feat && (!exact || sc->feat64)));
+  float* feat = in_place ? sc->feat : nullptr;
+  double* feat64 = in_place ? sc->feat64 : nullptr;
+  if (!in_place && n > 0 && D > 0) {
+    cudaError_t e = cudaMalloc(&feat, sizeof(float) * n * D);
+    if (e == cudaSuccess && exact) e = cudaMalloc(&feat64, sizeof(double) * n * D);
+    if (e != cudaSuccess) {
+      cudaFree(feat);
+      return psm::fail_cuda(ctx, e, "assign_labels feature rows", __FILE__, __LINE__);
+    }
   }
+  double *dqtab = nullptr, *scratch = nullptr, *ddist = nullptr;
+  int32_t *didx = nullptr, *darg = nullptr;
+  PSM_TRY(psm::ensure(ctx, ctx->lab_tmp, qtab.size() + static_cast<size_t>(na) + (nq > 0 ? nq : 1), &dqtab));
+  didx = reinterpret_cast<int32_t*>(dqtab + qtab.size());
+  PSM_CUDA_TRY(cudaMemcpyAsync(dqtab, qtab.data(), sizeof(double) * qtab.size(), cudaMemcpyHostToDevice, st));
+  if (na > 0)
+    PSM_CUDA_TRY(cudaMemcpyAsync(didx, alive_index.data(), sizeof(int32_t) * na, cudaMemcpyHostToDevice, st));
+  PSM_CUDA_TRY(cudaMemcpyAsync(didx + na, alive_slot.data(), sizeof(int32_t) * (nq > 0 ? nq : 1),
+                               cudaMemcpyHostToDevice, st));
+  if (n > 0 && na > 0) PSM_TRY(psm::ensure(ctx, ctx->lab_scratch, static_cast<size_t>(n) * na, &scratch));
+  if (n > 0 && dist_out && nq > 0) PSM_TRY(psm::ensure(ctx, ctx->lab_dist, static_cast<size_t>(n) * nq, &ddist));
+  if (n > 0 && argmax_out) PSM_TRY(psm::ensure(ctx, ctx->lab_arg, static_cast<size_t>(n), &darg));
   psm::LabelParams lp;
   lp.n = n;
   lp.c_sem = sc->c_sem;
@@ -802,34 +803,28 @@ int psm_assign_labels(psm_ctx* ctx, psm_scene* sc, const psm_queries* qs, double
   lp.scratch = scratch;
   lp.dist = ddist;
   lp.argmax = darg;
-  if (n > 0 && (D > 0 || argmax_out)) {
-    if (c_ins > 0 && !sc->f_ins) {
-      cleanup();
-      cudaFree(feat);
-      cudaFree(feat64);
-      return fail(ctx, PSM_EINVAL, "assign_labels: the scene has no f_ins");
+  if (n > 0 && na > 0 && c_ins > 0 && !sc->f_ins) {
+    if (!in_place) { cudaFree(feat); cudaFree(feat64); }
+    return fail(ctx, PSM_EINVAL, "assign_labels: the scene has no f_ins");
+  }
+  if (n > 0 && (D > 0 || darg)) psm::launch_assign_labels(lp, st);
+  PSM_CUDA_TRY(cudaGetLastError());
+  if (!in_place) {  // retire the old rows once the kernel has read them
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+    if (n > 0 && D > 0) {
+      cudaFree(sc->feat);
+      cudaFree(sc->feat64);
+      sc->feat = feat;
+      sc->feat64 = feat64;
     }
-    if (D > 0 || darg) psm::launch_assign_labels(lp, ctx->stream);
-  }
-  e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  if (e == cudaSuccess && ddist) e = cudaMemcpy(dist_out, ddist, sizeof(double) * n * nq, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && darg) e = cudaMemcpy(argmax_out, darg, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && argmax_out && n > 0 && na == 0)
-    for (int64_t i = 0; i < n; ++i) argmax_out[i] = -1;
-  cleanup();
-  if (e != cudaSuccess) {
-    cudaFree(feat);
-    cudaFree(feat64);
-    return psm::fail_cuda(ctx, e, "assign_labels", __FILE__, __LINE__);
-  }
-  if (n > 0 && D > 0) {
-    cudaFree(sc->feat);
-    cudaFree(sc->feat64);
-    sc->feat = feat;
-    sc->feat64 = feat64;
   }
   sc->n_q = nq;
+  if (ddist) PSM_CUDA_TRY(cudaMemcpyAsync(dist_out, ddist, sizeof(double) * n * nq, cudaMemcpyDeviceToHost, st));
+  if (darg) PSM_CUDA_TRY(cudaMemcpyAsync(argmax_out, darg, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+  if (dist_out || argmax_out) PSM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (argmax_out && n > 0 && na == 0)
+    for (int64_t i = 0; i < n; ++i) argmax_out[i] = -1;
+  if (dist_out && nq > 0 && n > 0 && !ddist) std::memset(dist_out, 0, sizeof(double) * n * nq);
   return PSM_OK;
 }
 

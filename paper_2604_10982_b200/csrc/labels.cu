@@ -16,30 +16,29 @@
 namespace psm {
 namespace {
 
-__global__ void __launch_bounds__(256) assign_labels_kernel(LabelParams p) {
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= p.n) return;
+// Copies the alive-query table (features, means, inverse covariances: n_alive x
+// (c_ins + 12) doubles) and psm_exp's table into shared memory.
+__device__ __forceinline__ void stage_tables(const LabelParams& p, double* qs, uint64_t* tab) {
+  const int words = p.n_alive * (p.c_ins + 12);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) qs[i] = p.q_feat[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = psm_exp_tab_dev[i];
+  __syncthreads();
+}
+
+// The surfel's new row: f_sem columns (when not in place), then dist over all queries.
+__device__ __forceinline__ void write_rows(const LabelParams& p, int64_t s, int best) {
   const int D = p.c_sem + p.n_q;
   float* row32 = p.feat_out + s * D;
   double* row64 = p.feat64_out ? p.feat64_out + s * D : nullptr;
-  // f_sem columns carried over from the old rows
-  for (int c = 0; c < p.c_sem; ++c) {
+  // f_sem columns carried over from the old rows (nothing to do when rewriting in place)
+  for (int c = 0; c < (p.feat_out == p.feat_in ? 0 : p.c_sem); ++c) {
     row32[c] = p.feat_in[s * p.d_in + c];
     if (row64) row64[c] = p.feat64_in[s * p.d_in + c];
   }
-  int best = -1;
-  if (p.n_alive > 0) {
-    double center[3];
-    center[0] = p.surfels[s * 13 + 0];
-    center[1] = p.surfels[s * 13 + 1];
-    center[2] = p.surfels[s * 13 + 2];
-    const int b = psm_assign_one(p.f_ins + s * p.c_ins, p.c_ins, center, p.n_alive, p.q_feat, p.q_mean, p.q_inv,
-                                 p.scratch + s, p.n, psm_exp_tab_dev);
-    best = p.alive_index[b];
-  }
   for (int q = 0; q < p.n_q; ++q) {
     const int a = p.alive_slot[q];
-    const double v = a >= 0 ? p.scratch[static_cast<int64_t>(a) * p.n + s] : 0.0;
+    double v = 0.0;
+    if (a >= 0) v = p.scratch[static_cast<int64_t>(a) * p.n + s];
     row32[p.c_sem + q] = static_cast<float>(v);
     if (row64) row64[p.c_sem + q] = v;
     if (p.dist) p.dist[s * p.n_q + q] = v;
@@ -47,12 +46,51 @@ __global__ void __launch_bounds__(256) assign_labels_kernel(LabelParams p) {
   if (p.argmax) p.argmax[s] = best;
 }
 
+// General path: A values in the column-major global scratch (a * N + s); the query
+// table in shared memory when it fits (kQsWords), else read through L1.
+constexpr int kQsWords = 6144;  // 48 KB
+__global__ void __launch_bounds__(256) assign_labels_kernel(LabelParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* tab = reinterpret_cast<uint64_t*>(smem);
+  double* qs = reinterpret_cast<double*>(smem + 2048);
+  const bool staged = p.n_alive * (p.c_ins + 12) <= kQsWords;
+  if (staged) {
+    stage_tables(p, qs, tab);
+  } else {
+    tab[threadIdx.x] = psm_exp_tab_dev[threadIdx.x];
+    __syncthreads();
+  }
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= p.n) return;
+  const double* fq = staged ? qs : p.q_feat;
+  const double* mean = fq + p.n_alive * p.c_ins;
+  const double* inv = mean + 3 * p.n_alive;
+  int best = -1;
+  if (p.n_alive > 0) {
+    const double center[3] = {p.surfels[s * 13 + 0], p.surfels[s * 13 + 1], p.surfels[s * 13 + 2]};
+    const int b = psm_assign_one(p.f_ins + s * p.c_ins, p.c_ins, center, p.n_alive, fq, mean, inv,
+                                 p.scratch + s, p.n, tab);
+    best = p.alive_index[b];
+  }
+  write_rows(p, s, best);
+}
+
 }  // namespace
 
 void launch_assign_labels(const LabelParams& p, cudaStream_t st) {
   if (p.n <= 0) return;
+  static unsigned long long configured = 0;  // one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured >> dev & 1ull)) {
+    const int most = 2048 + static_cast<int>(sizeof(double)) * kQsWords;
+    cudaFuncSetAttribute(assign_labels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+    configured |= 1ull << dev;
+  }
   const unsigned blocks = static_cast<unsigned>((p.n + 255) / 256);
-  assign_labels_kernel<<<blocks, 256, 0, st>>>(p);
+  const int words = p.n_alive * (p.c_ins + 12);
+  const size_t smem = 2048 + (words <= kQsWords ? sizeof(double) * words : 0);
+  assign_labels_kernel<<<blocks, 256, smem, st>>>(p);
 }
 
 }  // namespace psm

@@ -114,8 +114,9 @@ PSM_PHD int psm_assign_one(const double* f_ins, int c_ins, const double* center,
     a_vals[a * a_stride] = av;
     a_max = av > a_max ? av : a_max;  // std::max(a_max, av)
   }
+  // exp(A - A_max) is evaluated once per query (the reference evaluates the same
+  // argument twice, panoptic.cpp:79,83; exp is deterministic, so the values agree)
   double denom = 0;
-  for (int a = 0; a < n_alive; ++a) denom += psm_exp_t(a_vals[a * a_stride] - a_max, tab);
   int best = 0;
   double best_a = a_vals[0];
   for (int a = 0; a < n_alive; ++a) {
@@ -124,8 +125,11 @@ PSM_PHD int psm_assign_one(const double* f_ins, int c_ins, const double* center,
       best = a;
       best_a = av;
     }
-    a_vals[a * a_stride] = psm_exp_t(av - a_max, tab) / denom;
+    const double e = psm_exp_t(av - a_max, tab);
+    a_vals[a * a_stride] = e;
+    denom += e;
   }
+  for (int a = 0; a < n_alive; ++a) a_vals[a * a_stride] = a_vals[a * a_stride] / denom;
   return best;
 }
 

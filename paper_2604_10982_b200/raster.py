@@ -264,31 +264,49 @@ class Renderer:
         (render_panoptic reproduces the reference's argmaxes bit for bit)."""
         return DeviceScene(self, scene, labels, exact)
 
-    def assign_labels(self, dscene: DeviceScene, queries) -> Tuple[np.ndarray, np.ndarray]:
+    def assign_labels(self, dscene: DeviceScene, queries, outputs: bool = True):
         """assign_labels (panoptic.cpp:36-91) on the GPU: the scene's label channels become
-        the per-surfel distribution over `queries`. Returns (dist (N, Q), argmax (N,))."""
+        the per-surfel distribution over `queries`. Returns (dist (N, Q), argmax (N,)); with
+        outputs=False nothing is copied back and the call is asynchronous on the context stream."""
         from .panoptic import pack_queries
         lib = _lib.load()
         feat, mean, cov, alive, cls = pack_queries(queries, dscene.c_ins)
         q = len(queries)
         qs = A.psm_queries(q, dscene.c_ins, _ptr(feat), _ptr(mean), _ptr(cov), _ptr(alive), _ptr(cls))
-        dist = np.zeros((dscene.n, q))
-        arg = np.full(dscene.n, -1, np.int32)
+        dist = np.zeros((dscene.n, q)) if outputs else None
+        arg = np.full(dscene.n, -1, np.int32) if outputs else None
         _check(lib.psm_assign_labels(self.ctx, dscene.handle, C.byref(qs), _ptr(dist), _ptr(arg)), self.ctx,
                "assign_labels")
         dscene.n_q = q
-        return dist, arg
+        return (dist, arg) if outputs else None
+
+    def render_panoptic_device(self, dscene: DeviceScene, cam: Camera, cfg: RasterConfig, query_class: np.ndarray,
+                               planes: dict, counters: bool = False):
+        """render_panoptic into device int32 planes {"ids", "classes", "sem_classes": device pointer};
+        asynchronous unless counters are asked for."""
+        lib = _lib.load()
+        qc = np.ascontiguousarray(np.asarray(query_class, dtype=np.int32))
+        pt = A.psm_panoptic_targets(planes.get("ids"), planes.get("classes"), planes.get("sem_classes"), 1)
+        cnt = A.psm_counters()
+        c_cam, c_cfg = cam.to_c(), cfg.to_c()
+        _check(lib.psm_render_panoptic(self.ctx, dscene.handle, C.byref(c_cam), C.byref(c_cfg), _ptr(qc), qc.size,
+                                       C.byref(pt), C.byref(cnt) if counters else None), self.ctx, "render_panoptic")
+        return cnt if counters else None
 
     def render_panoptic(self, dscene: DeviceScene, cam: Camera, cfg: RasterConfig, query_class,
-                        counters: bool = False):
+                        counters: bool = False, out=None):
         """render_panoptic (metrics.cpp:339-369) over a DeviceScene whose labels are assigned
-        (assign_labels or uploaded): PanopticRender of (H, W, 1) int32 planes."""
+        (assign_labels or uploaded): PanopticRender of (H, W, 1) int32 planes. `out` (a
+        PanopticRender of matching shape, e.g. over pinned memory) is reused when given."""
         from .panoptic import PanopticRender
         lib = _lib.load()
         h, w = cam.height, cam.width
-        ids = np.empty((h, w, 1), np.int32)
-        classes = np.empty((h, w, 1), np.int32)
-        sem = np.empty((h, w, 1), np.int32)
+        if out is not None and out.ids.shape == (h, w, 1):
+            ids, classes, sem = out.ids, out.classes, out.sem_classes
+        else:
+            ids = np.empty((h, w, 1), np.int32)
+            classes = np.empty((h, w, 1), np.int32)
+            sem = np.empty((h, w, 1), np.int32)
         qc = np.ascontiguousarray(np.asarray(list(query_class), dtype=np.int32))
         pt = A.psm_panoptic_targets(_ptr(ids), _ptr(classes), _ptr(sem), 0)
         cnt = A.psm_counters()
