@@ -69,6 +69,7 @@ struct MatX {
   double& operator()(int r, int c) { return data_[static_cast<size_t>(c) * rows_ + r]; }
   double operator()(int r, int c) const { return data_[static_cast<size_t>(c) * rows_ + r]; }
   const double* data() const { return data_.data(); }
+  double* data() { return data_.data(); }
 };
 
 struct Surfel {  // core_types.hpp:17-25
@@ -123,10 +124,20 @@ struct Camera {  // core_types.hpp:36-53
   }
 };
 
-struct SceneMap {  // core_types.hpp:102-111 (render-relevant part)
+struct InstanceQuery {  // core_types.hpp:76-84
+  VecX feature;                 // C_ins entries
+  Vec3 mean{};
+  Mat3 cov = Mat3::Identity();  // SPD
+  int class_id = -1;
+  bool alive = true;
+};
+
+struct SceneMap {  // core_types.hpp:102-111 (render and panoptic part)
   std::vector<Surfel> surfels;
   std::vector<std::string> vocabulary;
+  std::vector<InstanceQuery> queries;
   int c_sem() const { return surfels.empty() ? 0 : static_cast<int>(surfels[0].f_sem.size()); }
+  int c_ins() const { return surfels.empty() ? 0 : static_cast<int>(surfels[0].f_ins.size()); }
 };
 
 template <typename T>
@@ -244,6 +255,61 @@ inline std::unique_ptr<UploadedScene> upload(const SceneMap& scene, const MatX* 
   return u;
 }
 
+// Upload with f_ins and fp64 feature copies (PSM_SCENE_EXACT_FEATURES), for the panoptic layer.
+inline std::unique_ptr<UploadedScene> upload_exact(const SceneMap& scene, psm_ctx* ctx) {
+  const int64_t n = static_cast<int64_t>(scene.surfels.size());
+  const int c_sem = scene.c_sem(), c_ins = scene.c_ins();
+  std::vector<double> geo(static_cast<size_t>(n) * 13), fs(static_cast<size_t>(n) * c_sem),
+      fi(static_cast<size_t>(n) * c_ins);
+  for (int64_t i = 0; i < n; ++i) {
+    const Surfel& s = scene.surfels[i];
+    double* g = &geo[static_cast<size_t>(i) * 13];
+    for (int k = 0; k < 3; ++k) g[k] = s.center[k];
+    for (int k = 0; k < 4; ++k) g[3 + k] = s.rotation[k];
+    g[7] = s.scales[0]; g[8] = s.scales[1]; g[9] = s.opacity;
+    for (int k = 0; k < 3; ++k) g[10 + k] = s.color[k];
+    for (int c = 0; c < c_sem; ++c) fs[static_cast<size_t>(i) * c_sem + c] = s.f_sem[c];
+    for (int c = 0; c < c_ins; ++c) fi[static_cast<size_t>(i) * c_ins + c] = s.f_ins[c];
+  }
+  auto u = std::make_unique<UploadedScene>();
+  u->ctx = ctx;
+  psm_scene_desc d{geo.data(), n, fs.data(), c_sem, nullptr, 0, fi.data(), c_ins, PSM_SCENE_EXACT_FEATURES};
+  check(psm_scene_create(ctx, &d, &u->sc), ctx);
+  return u;
+}
+
+// Flat query arrays for psm_queries (features from `features` columns when given).
+struct QueryArrays {
+  std::vector<double> feat, mean, cov;
+  std::vector<int32_t> alive, cls;
+  psm_queries view(int c_ins) const {
+    return psm_queries{static_cast<int32_t>(alive.size()), c_ins, feat.data(), mean.data(), cov.data(),
+                       alive.data(), cls.data()};
+  }
+};
+inline QueryArrays flatten(const std::vector<InstanceQuery>& qs, const MatX* features, int c_ins) {
+  QueryArrays a;
+  const size_t q = qs.size();
+  a.feat.resize(q * c_ins);
+  a.mean.resize(q * 3);
+  a.cov.resize(q * 9);
+  a.alive.resize(q);
+  a.cls.resize(q);
+  for (size_t i = 0; i < q; ++i) {
+    for (int c = 0; c < c_ins; ++c) {
+      const double v = features ? (*features)(c, static_cast<int>(i)) : qs[i].feature[c];
+      a.feat[i * c_ins + c] = v;
+    }
+    if (!features && static_cast<int>(qs[i].feature.size()) != c_ins)
+      throw std::invalid_argument("feature_similarity: dimension mismatch");  // panoptic.cpp:12-14
+    for (int k = 0; k < 3; ++k) a.mean[i * 3 + k] = qs[i].mean[k];
+    std::copy(qs[i].cov.m.begin(), qs[i].cov.m.end(), a.cov.begin() + i * 9);
+    a.alive[i] = qs[i].alive ? 1 : 0;
+    a.cls[i] = qs[i].class_id;
+  }
+  return a;
+}
+
 template <typename T>
 inline void reset_plane(Plane<T>& p, int w, int h, int c) {  // raster.cpp:255-262
   if (p.width != w || p.height != h || p.channels != c) p = Plane<T>(w, h, c);
@@ -342,6 +408,58 @@ inline BenchReport bench_render(const SceneMap& scene, const MatX* labels, const
   }
   psm_set_profiling(ctx, 0);
   return report;
+}
+
+struct LabelAssignment {  // panoptic.hpp:28-31
+  MatX dist;                // N_queries x N_surfels, columns sum to 1
+  std::vector<int> argmax;  // ties to the lowest query index
+};
+
+// assign_labels (panoptic.cpp:36-91) on the GPU.
+inline LabelAssignment assign_labels(const std::vector<InstanceQuery>& queries, const MatX* features,
+                                     const SceneMap& scene) {
+  psm_ctx* ctx = b200::context();
+  auto up = b200::upload_exact(scene, ctx);
+  const int n_q = static_cast<int>(queries.size()), n_s = static_cast<int>(scene.surfels.size());
+  const b200::QueryArrays qa = b200::flatten(queries, features, scene.c_ins());
+  const psm_queries qv = qa.view(scene.c_ins());
+  LabelAssignment out;
+  out.dist = MatX(n_q, n_s);
+  std::vector<int32_t> arg(static_cast<size_t>(n_s), -1);
+  b200::check(psm_assign_labels(ctx, up->sc, &qv, out.dist.data(), arg.data()), ctx);
+  out.argmax.assign(arg.begin(), arg.end());
+  return out;
+}
+
+struct PanopticRender {  // metrics.hpp:70-78
+  IntPlane ids;
+  IntPlane classes;
+  IntPlane sem_classes;
+};
+
+// render_panoptic (metrics.cpp:339-369): assign_labels over scene.queries, render with
+// the label distribution, and the alpha >= 0.5 id / class / semantic-class epilogue,
+// fused into the GPU blend (bit-identical argmaxes).
+inline PanopticRender render_panoptic(const SceneMap& scene, const Camera& cam, const RasterConfig& cfg) {
+  psm_ctx* ctx = b200::context();
+  auto up = b200::upload_exact(scene, ctx);
+  const b200::QueryArrays qa = b200::flatten(scene.queries, nullptr, scene.c_ins());
+  if (!scene.queries.empty()) {
+    const psm_queries qv = qa.view(scene.c_ins());
+    b200::check(psm_assign_labels(ctx, up->sc, &qv, nullptr, nullptr), ctx);
+  }
+  PanopticRender out;
+  out.ids = IntPlane(cam.width, cam.height, 1, -1);
+  out.classes = IntPlane(cam.width, cam.height, 1, -1);
+  out.sem_classes = IntPlane(cam.width, cam.height, 1, -1);
+  psm_panoptic_targets pt{out.ids.data.data(), out.classes.data.data(), out.sem_classes.data.data(), 0};
+  const psm_camera cc = cam.to_c();
+  const psm_raster_config rc = cfg.to_c();
+  psm_counters counters{};
+  b200::check(psm_render_panoptic(ctx, up->sc, &cc, &rc, qa.cls.data(), static_cast<int32_t>(qa.cls.size()), &pt,
+                                  &counters),
+              ctx);
+  return out;
 }
 
 }  // namespace psimap

@@ -121,6 +121,40 @@ int main() {
     CHECK(r1.rows[2].blended_total == r1.rows[3].blended_total);
     std::printf("bench grid counters: %s\n", failures > f0 ? "FAIL" : "ok");
   }
+  {  // test_panoptic.cpp:93-112 through assign_labels, and render_panoptic's structure
+    const int f0 = failures;
+    SceneMap scene;
+    for (int i = 0; i < 6; ++i) {
+      Surfel s = facing_surfel(vec3(-0.3 + 0.12 * i, 0, 2.0 + 0.05 * i), 0.2, 0.2, 0.9, vec3(0.5, 0.5, 0.5));
+      s.f_ins = VecX{0.1 * i, -0.2};
+      scene.surfels.push_back(s);
+    }
+    InstanceQuery q;
+    q.feature = VecX{1.0, 1.0};
+    const LabelAssignment one = assign_labels({q}, nullptr, scene);
+    for (int s = 0; s < 6; ++s) CHECK(approx(one.dist(0, s), 1.0, 1e-12) && one.argmax[s] == 0);
+    const LabelAssignment two = assign_labels({q, q}, nullptr, scene);
+    for (int s = 0; s < 6; ++s) CHECK(approx(two.dist(1, s), 0.5, 1e-12) && two.argmax[s] == 0);
+    InstanceQuery a = q, b = q;
+    a.mean = vec3(-0.3, 0, 2.0);
+    a.cov = Mat3::Identity();
+    a.class_id = 4;
+    b.mean = vec3(0.3, 0, 2.25);
+    b.class_id = 7;
+    scene.queries = {a, b};
+    const Camera cam = front_camera(32, 32);
+    const PanopticRender pr = render_panoptic(scene, cam, RasterConfig());
+    int n_id = 0;
+    for (int y = 0; y < 32; ++y)
+      for (int x = 0; x < 32; ++x) {
+        const int id = pr.ids.at(x, y), cls = pr.classes.at(x, y);
+        CHECK(id >= -1 && id <= 1);
+        CHECK((id == -1 && cls == -1) || (id == 0 && cls == 4) || (id == 1 && cls == 7));
+        n_id += id >= 0;
+      }
+    CHECK(n_id > 0);
+    std::printf("assign_labels / render_panoptic: %s\n", failures > f0 ? "FAIL" : "ok");
+  }
   std::printf("%d failures\n", failures);
   return failures;
 }
