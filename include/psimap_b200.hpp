@@ -128,14 +128,24 @@ struct InstanceQuery {  // core_types.hpp:76-84
   VecX feature;                 // C_ins entries
   Vec3 mean{};
   Mat3 cov = Mat3::Identity();  // SPD
+  std::vector<int64_t> class_votes;
   int class_id = -1;
+  int64_t assign_count = 0;
   bool alive = true;
 };
 
-struct SceneMap {  // core_types.hpp:102-111 (render and panoptic part)
+struct AttentionWeights {  // core_types.hpp:89-100 (carried through checkpoints; not used by render)
+  MatX w_q, w_k, w_v;  // C_ins x d
+  int pos_enc_bands = 6;
+  double pos_enc_base_freq = 0.5;
+  uint64_t pos_enc_seed = 42;
+};
+
+struct SceneMap {  // core_types.hpp:102-111
   std::vector<Surfel> surfels;
   std::vector<std::string> vocabulary;
   std::vector<InstanceQuery> queries;
+  AttentionWeights attn;
   int c_sem() const { return surfels.empty() ? 0 : static_cast<int>(surfels[0].f_sem.size()); }
   int c_ins() const { return surfels.empty() ? 0 : static_cast<int>(surfels[0].f_ins.size()); }
 };
@@ -408,6 +418,52 @@ inline BenchReport bench_render(const SceneMap& scene, const MatX* labels, const
   }
   psm_set_profiling(ctx, 0);
   return report;
+}
+
+struct StreetSpec {  // synthetic.hpp (make_street_scene parameters)
+  int n_surfels = 12000;
+  uint64_t seed = 7;
+  double min_aspect = 5.0;
+  int image_w = 256, image_h = 192;
+  int c_sem = 16;
+  int n_instances = 256;
+  double scale_mult = 1.0;  // extension: s1 multiplier (1 = the reference's scales)
+};
+struct StreetScene {
+  SceneMap scene;
+  MatX labels;  // n_instances x N near one-hot
+  Camera camera;
+};
+
+// make_street_scene (synthetic.cpp:236-312), generated by libpsm's host code.
+inline StreetScene make_street_scene(const StreetSpec& spec) {
+  psm_street_spec cs{spec.n_surfels, spec.seed, spec.min_aspect, spec.image_w, spec.image_h, spec.c_sem,
+                     spec.n_instances, spec.scale_mult};
+  int64_t n = 0;
+  psm_camera cam{};
+  if (psm_make_street_scene(&cs, &n, nullptr, nullptr, nullptr, &cam) != PSM_OK)
+    throw std::invalid_argument("make_street_scene: bad spec");
+  std::vector<double> geo(static_cast<size_t>(n) * 13), fs(static_cast<size_t>(n) * spec.c_sem),
+      fi(static_cast<size_t>(n) * 8);
+  StreetScene out;
+  out.labels = MatX(spec.n_instances, static_cast<int>(n));
+  b200::check(psm_make_street_scene(&cs, &n, geo.data(), fs.data(), out.labels.data(), &cam), nullptr);
+  b200::check(psm_make_street_scene_ins(&cs, &n, fi.data()), nullptr);
+  out.camera = Camera::from_c(cam);
+  out.scene.vocabulary = {"street"};
+  out.scene.surfels.resize(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    Surfel& s = out.scene.surfels[static_cast<size_t>(i)];
+    const double* g = &geo[static_cast<size_t>(i) * 13];
+    for (int k = 0; k < 3; ++k) s.center[k] = g[k];
+    for (int k = 0; k < 4; ++k) s.rotation[k] = g[3 + k];
+    s.scales = vec2(g[7], g[8]);
+    s.opacity = g[9];
+    for (int k = 0; k < 3; ++k) s.color[k] = g[10 + k];
+    s.f_sem.assign(fs.begin() + i * spec.c_sem, fs.begin() + (i + 1) * spec.c_sem);
+    s.f_ins.assign(fi.begin() + i * 8, fi.begin() + (i + 1) * 8);
+  }
+  return out;
 }
 
 struct LabelAssignment {  // panoptic.hpp:28-31
