@@ -235,6 +235,32 @@ int psm_render_panoptic(psm_ctx* ctx, const psm_scene* scene, const psm_camera* 
                         const psm_raster_config* cfg, const int32_t* query_class, int32_t n_query_class,
                         const psm_panoptic_targets* targets, psm_counters* counters);
 
+/* ---- Backward of the render --------------------------
+ * The blending backward of the training pipeline (proj/src/pipeline.cpp:347-460)
+ * and project_surfel_backward (raster.cpp:179-203): given dL/d(colour, semantic
+ * feature, label distribution) planes, the gradients of every surfel parameter.
+ * Depth and normal planes carry no gradient, as in the reference. */
+typedef struct psm_plane_grads {
+  const double* color;    /* W*H*3, NULL = 0 */
+  const double* sem_feat; /* W*H*C_sem, NULL = 0 */
+  const double* ins_dist; /* W*H*N_q, NULL = 0 */
+} psm_plane_grads;
+
+typedef struct psm_scene_grads { /* host outputs, each may be NULL */
+  double* opacity;  /* N */
+  double* color;    /* N*3 */
+  double* f_sem;    /* N*C_sem */
+  double* labels;   /* N*N_q (per surfel, the MatX column) */
+  double* center;   /* N*3 */
+  double* rotation; /* N*4 (w, x, y, z) */
+  double* scales;   /* N*2 */
+} psm_scene_grads;
+
+/* Re-runs the forward (recording each pixel's contributors) and back-propagates.
+ * Synchronous. Gradients are sums over pixels in an unspecified order (fp64 atomics). */
+int psm_render_backward(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam,
+                        const psm_raster_config* cfg, const psm_plane_grads* grads, psm_scene_grads* out);
+
 /* Workload: make_street_scene (proj/src/synthetic.cpp:236-312) with the same
  * RNG draw order, plus `scale_mult` applied to s1 after it is drawn
  * (density-normalised variants; 1.0 = verbatim). Two-phase:

@@ -17,6 +17,8 @@
 //   include/psimap/core_types.hpp:51-52  Camera::to_camera, center_world
 //   src/panoptic.cpp:36-91   assign_labels (math in psm_panoptic.h, shared with the GPU)
 //   src/metrics.cpp:339-369  render_panoptic epilogue (oracle/pyoracle.py, over render's fp64 planes)
+//   src/pipeline.cpp:347-460 blending backward, raster.cpp:179-203 project_surfel_backward
+//                            (oracle_render_backward; geometry chain in psm_backward.h)
 //
 // Why a restatement: the reference needs Eigen3, which is not in this image
 // (proj/CMakeLists.txt:13-15 `find_path(EIGEN3_INCLUDE_DIR ... REQUIRED)`), so
@@ -48,6 +50,7 @@
 #include "../paper_2604_10982_b200/csrc/psm_ellipse.h"
 #include "../paper_2604_10982_b200/csrc/psm_exp.h"
 #include "../paper_2604_10982_b200/csrc/psm_panoptic.h"
+#include "../paper_2604_10982_b200/csrc/psm_backward.h"
 
 namespace {
 
@@ -525,11 +528,21 @@ typedef struct oracle_cache {
   int64_t cap;
 } oracle_cache;
 
+// Backward state (pipeline.cpp:347-460): upstream plane gradients in, per-surfel sums out.
+struct BackwardAcc {
+  const psm_plane_grads* g;
+  std::vector<double> opacity, color, fsem, lab, hinv;  // per source; hinv per projected (row-major)
+  std::vector<double> center, rotation, scales;         // per source
+};
+
 static int render_impl(const double* surfels13, int64_t n, const double* f_sem, int32_t c_sem,
-                       const double* labels, int32_t n_q, const psm_camera* pcam, const psm_raster_config* cfg,
+                       const double* labels, int32_t n_q, const psm_camera* pcam, const psm_raster_config* cfg_in,
                        double* color, double* depth, double* normal, double* sem_feat, double* ins_dist,
                        int32_t* ins_argmax, double* alpha_acc, int32_t* blend_count, psm_counters* counters,
-                       psm_debug* dbg, oracle_stats* stats, oracle_cache* cache) {
+                       psm_debug* dbg, oracle_stats* stats, oracle_cache* cache, BackwardAcc* bwd = nullptr) {
+  psm_raster_config cfg_local = *cfg_in;
+  if (bwd) cfg_local.threads = 1;  // the backward sums into shared arrays: one deterministic pass
+  const psm_raster_config* cfg = &cfg_local;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
   const Cam cam = cam_from(pcam);
@@ -596,6 +609,7 @@ static int render_impl(const double* surfels13, int64_t n, const double* f_sem, 
       hot_normal[static_cast<size_t>(i) * 3 + c] = pr.normal_vis[c];
     }
   }
+  if (bwd) bwd->hinv.assign(static_cast<size_t>(n_proj) * 9, 0.0);
   const double rd_bg0 = cfg->background[0], rd_bg1 = cfg->background[1], rd_bg2 = cfg->background[2];
   std::vector<std::vector<std::pair<int, double>>> cache_rows(cache ? npx : 0);
   const bool rdn = cfg->render_depth_normal != 0;
@@ -692,6 +706,62 @@ static int render_impl(const double* surfels13, int64_t n, const double* f_sem, 
             for (int i = 0; i < k_sel; ++i) slot[i] = i < blend_n ? projected[blend_list[i].proj].source : -1;
           }
 
+          if (bwd && m > 0) {  // blending backward over this pixel (pipeline.cpp:378-453)
+            const double* gc = bwd->g->color ? bwd->g->color + 3 * pix : nullptr;
+            const double* gf = (c_sem > 0 && bwd->g->sem_feat) ? bwd->g->sem_feat + pix * c_sem : nullptr;
+            const double* gi = (n_q > 0 && bwd->g->ins_dist) ? bwd->g->ins_dist + pix * n_q : nullptr;
+            const double zero3[3] = {0, 0, 0};
+            if (!gc) gc = zero3;
+            std::vector<double> t_chain(m + 1, 1.0), wbuf(m);
+            for (int j = 0; j < m; ++j) {
+              wbuf[j] = scratch.entries[j].alpha * t_chain[j];
+              t_chain[j + 1] = t_chain[j] * (1.0 - scratch.entries[j].alpha);
+            }
+            const bool sel_all = !(topk && m > k_sel);
+            double suffix = t_chain[m] * (gc[0] * rd_bg0 + gc[1] * rd_bg1 + gc[2] * rd_bg2);
+            for (int j = m - 1; j >= 0; --j) {
+              const auto& e = scratch.entries[j];
+              const int64_t src = projected[e.proj].source;
+              const double* sf = surfels13 + 13 * src;
+              const double w_j = wbuf[j];
+              double direct = gc[0] * sf[10] + gc[1] * sf[11] + gc[2] * sf[12];
+              for (int c = 0; c < 3; ++c) bwd->color[src * 3 + c] += w_j * gc[c];
+              if (sel_all || scratch.selected[j]) {
+                if (gf) {
+                  double dot = 0;
+                  for (int i = 0; i < c_sem; ++i) {
+                    dot += gf[i] * f_sem[src * c_sem + i];
+                    bwd->fsem[src * c_sem + i] += w_j * gf[i];
+                  }
+                  direct += dot;
+                }
+                if (gi) {
+                  double dot = 0;
+                  for (int i = 0; i < n_q; ++i) {
+                    dot += gi[i] * labels[src * n_q + i];
+                    bwd->lab[src * n_q + i] += w_j * gi[i];
+                  }
+                  direct += dot;
+                }
+              }
+              const double one_minus = 1.0 - e.alpha;
+              const double g_alpha = t_chain[j] * direct - (one_minus > 0 ? suffix / one_minus : 0.0);
+              suffix += w_j * direct;
+              const double d_sigma = oexp(-0.5 * (e.u * e.u + e.v * e.v));
+              bwd->opacity[src] += d_sigma * g_alpha;
+              const double g_dsigma = sf[9] * g_alpha;
+              const double g_u = -e.u * d_sigma * g_dsigma;
+              const double g_v = -e.v * d_sigma * g_dsigma;
+              const HotGeom& hg = hot_geom[e.proj];
+              const double w2 = hg.h[6] * rx + hg.h[7] * ry + hg.h[8];
+              const double gw[3] = {g_u / w2, g_v / w2, -(e.u * g_u + e.v * g_v) / w2};
+              const double ray[3] = {rx, ry, 1.0};
+              double* gh = &bwd->hinv[static_cast<size_t>(e.proj) * 9];
+              for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) gh[r * 3 + c] += gw[r] * ray[c];
+            }
+          }
+
           const int feat_dims = c_sem + n_q;
           blends += blend_n;
           if (feat_dims > 0 && blend_n > 0) {
@@ -734,6 +804,20 @@ static int render_impl(const double* surfels13, int64_t n, const double* f_sem, 
   });
   const auto t3 = clk::now();
 
+  if (bwd) {  // project_surfel_backward per projected surfel (pipeline.cpp:478-486)
+    bwd->center.assign(static_cast<size_t>(n) * 3, 0.0);
+    bwd->rotation.assign(static_cast<size_t>(n) * 4, 0.0);
+    bwd->scales.assign(static_cast<size_t>(n) * 2, 0.0);
+    for (int i = 0; i < n_proj; ++i) {
+      const int64_t src = projected[i].source;
+      double dc[3], dq[4], ds[2];
+      psm_geom_backward(surfels13 + 13 * src, cam.r.m, hot_geom[i].h, &bwd->hinv[static_cast<size_t>(i) * 9], dc, dq,
+                        ds);
+      for (int k = 0; k < 3; ++k) bwd->center[src * 3 + k] += dc[k];
+      for (int k = 0; k < 4; ++k) bwd->rotation[src * 4 + k] += dq[k];
+      for (int k = 0; k < 2; ++k) bwd->scales[src * 2 + k] += ds[k];
+    }
+  }
   const uint64_t blended_total = std::accumulate(tile_blend.begin(), tile_blend.end(), uint64_t{0});
   if (counters) {
     counters->rn_total = grid.rn_total;
@@ -809,6 +893,39 @@ int oracle_render_cache(const double* surfels13, int64_t n, const double* f_sem,
                         oracle_cache* cache) {
   return render_impl(surfels13, n, f_sem, c_sem, labels, n_q, pcam, cfg, color, nullptr, nullptr, sem_feat, nullptr,
                      ins_argmax, nullptr, blend_count, nullptr, nullptr, nullptr, cache);
+}
+
+// Blending backward + geometry chain (pipeline.cpp:347-486) on the oracle.
+int oracle_render_backward(const double* surfels13, int64_t n, const double* f_sem, int32_t c_sem,
+                           const double* labels, int32_t n_q, const psm_camera* pcam, const psm_raster_config* cfg,
+                           const psm_plane_grads* g, psm_scene_grads* out) {
+  if (n == 0) c_sem = 0;
+  if (labels == nullptr) n_q = 0;
+  BackwardAcc acc;
+  acc.g = g;
+  acc.opacity.assign(static_cast<size_t>(n), 0.0);
+  acc.color.assign(static_cast<size_t>(n) * 3, 0.0);
+  acc.fsem.assign(static_cast<size_t>(n) * c_sem, 0.0);
+  acc.lab.assign(static_cast<size_t>(n) * n_q, 0.0);
+  const int st = render_impl(surfels13, n, f_sem, c_sem, labels, n_q, pcam, cfg, nullptr, nullptr, nullptr, nullptr,
+                             nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &acc);
+  if (st != PSM_OK) return st;
+  if (acc.center.empty()) {
+    acc.center.assign(static_cast<size_t>(n) * 3, 0.0);
+    acc.rotation.assign(static_cast<size_t>(n) * 4, 0.0);
+    acc.scales.assign(static_cast<size_t>(n) * 2, 0.0);
+  }
+  auto put = [](double* dst, const std::vector<double>& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+  };
+  put(out->opacity, acc.opacity);
+  put(out->color, acc.color);
+  put(out->f_sem, acc.fsem);
+  put(out->labels, acc.lab);
+  put(out->center, acc.center);
+  put(out->rotation, acc.rotation);
+  put(out->scales, acc.scales);
+  return PSM_OK;
 }
 
 }  // extern "C"

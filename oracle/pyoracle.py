@@ -284,3 +284,30 @@ def render_panoptic(scene, f_ins, queries, cam, cfg) -> dict:
     pr = panoptic_epilogue(out["alpha_acc"], out["ins_argmax"], out["sem_feat"], [q.class_id for q in queries])
     out.update(ids=pr.ids, classes=pr.classes, sem_classes=pr.sem_classes, dist=dist, label_argmax=arg)
     return out
+
+
+def render_backward(scene, labels, cam, cfg, g_color=None, g_sem=None, g_ins=None) -> dict:
+    """Blending backward + project_surfel_backward (pipeline.cpp:347-486) on the oracle: gradients of
+    L = <g_color, colour> + <g_sem, sem_feat> + <g_ins, ins_dist> w.r.t. every surfel parameter."""
+    lib = load()
+    fn = lib.oracle_render_backward
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(A.psm_camera),
+                   C.POINTER(A.psm_raster_config), C.POINTER(A.psm_plane_grads), C.POINTER(A.psm_scene_grads)]
+    s = scene.surfels
+    n = s.shape[0]
+    c_sem = scene.c_sem()
+    lab = None if labels is None else np.ascontiguousarray(np.asarray(labels, dtype=np.float64))
+    n_q = 0 if lab is None else lab.shape[1]
+    gp = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in (g_color, g_sem, g_ins)]
+    out = {"opacity": np.zeros(n), "color": np.zeros((n, 3)), "f_sem": np.zeros((n, c_sem)),
+           "labels": np.zeros((n, n_q)), "center": np.zeros((n, 3)), "rotation": np.zeros((n, 4)),
+           "scales": np.zeros((n, 2))}
+    pg = A.psm_plane_grads(*[_p(a) for a in gp])
+    sg = A.psm_scene_grads(*[_p(out[k]) for k in ("opacity", "color", "f_sem", "labels", "center", "rotation",
+                                                    "scales")])
+    st = fn(_p(s), n, _p(scene.f_sem), c_sem, _p(lab), n_q, C.byref(cam.to_c()), C.byref(cfg.to_c()), C.byref(pg),
+            C.byref(sg))
+    if st != 0:
+        raise ValueError("oracle backward failed")
+    return out

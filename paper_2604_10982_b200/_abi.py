@@ -78,10 +78,20 @@ class psm_panoptic_targets(C.Structure):
     _fields_ = [("ids", C.c_void_p), ("classes", C.c_void_p), ("sem_classes", C.c_void_p), ("on_device", C.c_int32)]
 
 
+class psm_plane_grads(C.Structure):
+    _fields_ = [("color", C.c_void_p), ("sem_feat", C.c_void_p), ("ins_dist", C.c_void_p)]
+
+
+class psm_scene_grads(C.Structure):
+    _fields_ = [("opacity", C.c_void_p), ("color", C.c_void_p), ("f_sem", C.c_void_p), ("labels", C.c_void_p),
+                ("center", C.c_void_p), ("rotation", C.c_void_p), ("scales", C.c_void_p)]
+
+
 # Every symbol include/psm.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED_SYMBOLS = (
     "psm_default_config", "psm_create", "psm_destroy", "psm_last_error", "psm_set_profiling", "psm_get_stage_times",
     "psm_sync", "psm_scene_upload", "psm_scene_free", "psm_scene_info", "psm_render", "psm_render_debug",
     "psm_render_batch", "psm_last_counters", "psm_make_street_scene", "psm_camera_look_at", "psm_camera_make",
     "psm_scene_create", "psm_assign_labels", "psm_render_panoptic", "psm_make_street_scene_ins",
+    "psm_render_backward",
 )
