@@ -42,6 +42,8 @@ def load():
         "psm_render_panoptic": (C.c_int, [vp, vp, P(A.psm_camera), P(A.psm_raster_config), vp, C.c_int32,
                                           P(A.psm_panoptic_targets), P(A.psm_counters)]),
         "psm_make_street_scene_ins": (C.c_int, [P(A.psm_street_spec), P(C.c_int64), vp]),
+        "psm_render_backward": (C.c_int, [vp, vp, P(A.psm_camera), P(A.psm_raster_config), P(A.psm_plane_grads),
+                                          P(A.psm_scene_grads)]),
         "psm_render_batch": (C.c_int, [vp, vp, P(A.psm_camera), C.c_int32, P(A.psm_raster_config),
                                        P(A.psm_targets), P(A.psm_counters)]),
         "psm_last_counters": (C.c_int, [vp, P(A.psm_counters)]),

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
           if (m < p.list_cap) {
             p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(pos), __float_as_uint(wf));
             if constexpr (PANO_T > 0) p.lists_w[pix * p.list_cap + m] = wt;
+            if (p.lists_t) p.lists_t[pix * p.list_cap + m] = T;  // backward cache: T before this blend
           }
         }
         T *= 1.0 - alpha;
@@ -368,6 +369,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
     }
     if constexpr (FULL_LIST) {
       if (m > p.list_cap) atomicMax(p.list_overflow, m);
+      if constexpr (KMAX > 0) {  // backward cache: the selected list positions
+        if (p.topk_pos)
+          for (int i = 0; i < blend_n; ++i) p.topk_pos[pix * k_sel + i] = top_p[i * kThreads + tid];
+      }
     }
     // ins_argmax stays -1 unless labels were accumulated (raster.cpp:292,497)
     if (p.n_q == 0 || blend_n == 0 || NV == 0) p.ins_argmax[pix] = -1;
@@ -651,6 +656,13 @@ int blend_nch_for(int feat_dims) {
 
 void launch_blend(const BlendParams& p, int tiles, bool topk, cudaStream_t st) {
   if (tiles <= 0) return;
+  if (p.lists_t) {  // backward cache: contributor lists (+ Top-K positions), no feature phase
+    if (!topk) launch_t<0, true, 1, 0, 32, true>(p, tiles, st);
+    else if (blend_kmax_for(p.k_sel) == 8) launch_t<8, true, 1, 0, 32, true>(p, tiles, st);
+    else if (blend_kmax_for(p.k_sel) == 16) launch_t<16, true, 1, 0, 32, true>(p, tiles, st);
+    else launch_t<32, true, 1, 0, 32, true>(p, tiles, st);
+    return;
+  }
   if (p.pan_ids) {  // render_panoptic: fp64 blend-order feature phase and the three id planes
     if (!topk) launch_pano<0, true>(p, tiles, st);
     else if (blend_kmax_for(p.k_sel) == 8) launch_pano<8, false>(p, tiles, st);

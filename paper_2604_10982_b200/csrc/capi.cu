@@ -49,6 +49,7 @@ struct Planes {
   int32_t *pan_ids = nullptr, *pan_classes = nullptr, *pan_sem = nullptr;
   const int32_t* qclass = nullptr;
   int32_t n_qclass = 0;
+  bool cache = false;  // backward cache: per-pixel contributor lists with transmittance
 };
 
 }  // namespace psm
@@ -72,6 +73,7 @@ struct psm_ctx {
   psm::Buf recs, bins, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, kscratch2, valid, pos, keys_c, src_c, keys_s, src_s;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
   psm::Buf lists_w, pan_ids, pan_classes, pan_sem, qclass, lab_tmp, lab_scratch, lab_dist, lab_arg;
+  psm::Buf lists_t, topk_pos, bw_gin, bw_out;
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
   psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
@@ -298,7 +300,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->topk_dbg, npx * k_sel, &tk));
     bp.topk_dbg = tk;
   }
-  const bool full_list = !topk && feat_dims > 0;
+  const bool full_list = (!topk && feat_dims > 0) || pl.cache;
   if (full_list) {
     if (ctx->list_cap == 0) ctx->list_cap = 128;
     uint2* lists;
@@ -309,6 +311,16 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
       double* lw;
       PSM_TRY(ensure(ctx, ctx->lists_w, npx * ctx->list_cap, &lw));
       bp.lists_w = lw;
+    }
+    if (pl.cache) {
+      double* lt;
+      PSM_TRY(ensure(ctx, ctx->lists_t, npx * ctx->list_cap, &lt));
+      bp.lists_t = lt;
+      if (topk) {
+        int32_t* tk;
+        PSM_TRY(ensure(ctx, ctx->topk_pos, npx * k_sel, &tk));
+        bp.topk_pos = tk;
+      }
     }
   }
   if (pl.pan_ids) {
@@ -617,7 +629,8 @@ int psm_destroy(psm_ctx* ctx) {
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
                       &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,
                       &ctx->lists_w, &ctx->pan_ids, &ctx->pan_classes, &ctx->pan_sem, &ctx->qclass, &ctx->lab_tmp,
-                      &ctx->lab_scratch, &ctx->lab_dist, &ctx->lab_arg,
+                      &ctx->lab_scratch, &ctx->lab_dist, &ctx->lab_arg, &ctx->lists_t, &ctx->topk_pos, &ctx->bw_gin,
+                      &ctx->bw_out,
                       &ctx->plane_color, &ctx->plane_depth, &ctx->plane_normal, &ctx->plane_sem, &ctx->plane_ins,
                       &ctx->plane_arg, &ctx->plane_alpha, &ctx->plane_cnt};
   for (psm::Buf* b : bufs) psm::free_buf(*b);
@@ -825,6 +838,105 @@ int psm_assign_labels(psm_ctx* ctx, psm_scene* sc, const psm_queries* qs, double
   if (argmax_out && n > 0 && na == 0)
     for (int64_t i = 0; i < n; ++i) argmax_out[i] = -1;
   if (dist_out && nq > 0 && n > 0 && !ddist) std::memset(dist_out, 0, sizeof(double) * n * nq);
+  return PSM_OK;
+}
+
+int psm_render_backward(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
+                        const psm_plane_grads* g, psm_scene_grads* out) {
+  if (!ctx || !sc || !cam || !cfg || !g || !out) return PSM_EINVAL;
+  if (cam->width <= 0 || cam->height <= 0) return psm::fail(ctx, PSM_EINVAL, "camera: image size must be positive");
+  PSM_TRY(psm::check_config(ctx, cfg, sc->c_sem + sc->n_q));
+  PSM_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int64_t n = sc->n;
+  const int cs = sc->c_sem, nq = sc->n_q, W = cam->width, H = cam->height;
+  const size_t npx = static_cast<size_t>(W) * H;
+  // forward in cache mode (planes in context scratch), re-rendered until its buffers fit
+  psm::Planes pl{};
+  PSM_TRY(psm::ensure(ctx, ctx->plane_color, npx * 3, &pl.color));
+  PSM_TRY(psm::ensure(ctx, ctx->plane_depth, npx * 2, &pl.depth));
+  PSM_TRY(psm::ensure(ctx, ctx->plane_normal, npx * 3, &pl.normal));
+  PSM_TRY(psm::ensure(ctx, ctx->plane_alpha, npx, &pl.alpha));
+  PSM_TRY(psm::ensure(ctx, ctx->plane_arg, npx, &pl.arg));
+  PSM_TRY(psm::ensure(ctx, ctx->plane_cnt, npx, &pl.cnt));
+  pl.sem = nullptr;
+  pl.ins = nullptr;
+  pl.cache = true;
+  if (ctx->list_cap == 0) ctx->list_cap = 128;
+  for (int attempt = 0;; ++attempt) {
+    PSM_TRY(psm::render_impl(ctx, sc, cam, cfg, pl, nullptr));
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+    bool rerun = false;
+    PSM_TRY(psm::check_frame(ctx, &rerun));
+    if (!rerun) break;
+    if (attempt >= 3) return psm::fail(ctx, PSM_ENOMEM, "render buffers did not converge");
+  }
+  psm::finish_counters(ctx);
+  // upstream plane gradients to the device
+  const size_t n_gc = g->color ? npx * 3 : 0, n_gs = (g->sem_feat && cs > 0) ? npx * cs : 0,
+               n_gi = (g->ins_dist && nq > 0) ? npx * nq : 0;
+  double* gin = nullptr;
+  PSM_TRY(psm::ensure(ctx, ctx->bw_gin, n_gc + n_gs + n_gi + 1, &gin));
+  if (n_gc) PSM_CUDA_TRY(cudaMemcpyAsync(gin, g->color, sizeof(double) * n_gc, cudaMemcpyHostToDevice, st));
+  if (n_gs)
+    PSM_CUDA_TRY(cudaMemcpyAsync(gin + n_gc, g->sem_feat, sizeof(double) * n_gs, cudaMemcpyHostToDevice, st));
+  if (n_gi)
+    PSM_CUDA_TRY(cudaMemcpyAsync(gin + n_gc + n_gs, g->ins_dist, sizeof(double) * n_gi, cudaMemcpyHostToDevice, st));
+  // gradient accumulators: opacity, colour, f_sem, labels, H^-1 (summed), centre, quaternion, scales
+  const size_t nn = static_cast<size_t>(n);
+  const size_t o_op = 0, o_col = nn, o_fs = o_col + 3 * nn, o_lab = o_fs + cs * nn, o_h = o_lab + nq * nn,
+               o_c = o_h + 9 * nn, o_r = o_c + 3 * nn, o_s = o_r + 4 * nn, total = o_s + 2 * nn;
+  double* acc = nullptr;
+  PSM_TRY(psm::ensure(ctx, ctx->bw_out, total + 1, &acc));
+  PSM_CUDA_TRY(cudaMemsetAsync(acc, 0, sizeof(double) * (o_c + 1), st));
+  if (n > 0) {
+    psm::BackwardParams bp{};
+    bp.width = W;
+    bp.height = H;
+    bp.k_sel = cfg->top_k > 1 ? cfg->top_k : 1;
+    bp.topk = cfg->blending == PSM_BLEND_TOPK;
+    bp.list_cap = ctx->list_cap;
+    bp.c_sem = cs;
+    bp.n_q = nq;
+    bp.cam_cx = cam->cx; bp.cam_cy = cam->cy; bp.cam_fx = cam->fx; bp.cam_fy = cam->fy;
+    bp.bg0 = cfg->background[0]; bp.bg1 = cfg->background[1]; bp.bg2 = cfg->background[2];
+    bp.lists = static_cast<const uint2*>(ctx->lists.p);
+    bp.lists_t = static_cast<const double*>(ctx->lists_t.p);
+    bp.topk_pos = bp.topk ? static_cast<const int32_t*>(ctx->topk_pos.p) : nullptr;
+    bp.blend_count = pl.cnt;
+    bp.vals = static_cast<const uint32_t*>(ctx->tvals.p);
+    bp.recs = static_cast<const psm::SurfRec*>(ctx->recs.p);
+    bp.surfels = sc->surfels;
+    bp.feat64 = sc->feat64;
+    bp.feat32 = sc->feat;
+    bp.g_color = n_gc ? gin : nullptr;
+    bp.g_sem = n_gs ? gin + n_gc : nullptr;
+    bp.g_ins = n_gi ? gin + n_gc + n_gs : nullptr;
+    bp.d_opacity = acc + o_op;
+    bp.d_color = acc + o_col;
+    bp.d_fsem = acc + o_fs;
+    bp.d_lab = acc + o_lab;
+    bp.d_hinv = acc + o_h;
+    psm::launch_pixel_backward(bp, st);
+    PSM_CUDA_TRY(cudaGetLastError());
+    psm::DevCamera dc;
+    std::memcpy(dc.r, cam->r_cw, sizeof dc.r);
+    psm::launch_geom_backward(sc->surfels, bp.recs, static_cast<const int32_t*>(ctx->valid.p), n, dc, acc + o_h,
+                              acc + o_c, acc + o_r, acc + o_s, st);
+    PSM_CUDA_TRY(cudaGetLastError());
+  }
+  auto d2h = [&](double* dst, size_t off, size_t count) -> int {
+    if (dst && count) PSM_CUDA_TRY(cudaMemcpyAsync(dst, acc + off, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+    return PSM_OK;
+  };
+  PSM_TRY(d2h(out->opacity, o_op, nn));
+  PSM_TRY(d2h(out->color, o_col, 3 * nn));
+  PSM_TRY(d2h(out->f_sem, o_fs, cs * nn));
+  PSM_TRY(d2h(out->labels, o_lab, nq * nn));
+  PSM_TRY(d2h(out->center, o_c, 3 * nn));
+  PSM_TRY(d2h(out->rotation, o_r, 4 * nn));
+  PSM_TRY(d2h(out->scales, o_s, 2 * nn));
+  PSM_CUDA_TRY(cudaStreamSynchronize(st));
   return PSM_OK;
 }
 

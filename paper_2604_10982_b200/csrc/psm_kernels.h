@@ -34,7 +34,33 @@ struct BlendParams {
   int32_t *pan_ids, *pan_classes, *pan_sem;
   const int32_t* query_class;
   int32_t n_query_class;
+  // backward cache (RenderCache::pixels, raster.cpp:399-403): when lists_t != NULL the
+  // lists hold every contributor's list position with the transmittance before it, and
+  // topk_pos [W*H][k_sel] the selected positions (Top-K)
+  double* lists_t;
+  int32_t* topk_pos;
 };
+
+// render backward (pipeline.cpp:347-486), backward.cu
+struct BackwardParams {
+  int32_t width, height, k_sel, topk, list_cap, c_sem, n_q;
+  double cam_cx, cam_cy, cam_fx, cam_fy, bg0, bg1, bg2;
+  const uint2* lists;
+  const double* lists_t;
+  const int32_t* topk_pos;
+  const int32_t* blend_count;
+  const uint32_t* vals;
+  const SurfRec* recs;
+  const double* surfels;   // [N][13]
+  const double* feat64;    // [N][c_sem + n_q] or NULL (then feat32)
+  const float* feat32;
+  const double *g_color, *g_sem, *g_ins;  // upstream plane gradients (device), may be NULL
+  double *d_opacity, *d_color, *d_fsem, *d_lab, *d_hinv;  // [N], [N][3], [N][c_sem], [N][n_q], [N][9]
+};
+void launch_pixel_backward(const BackwardParams& p, cudaStream_t st);
+void launch_geom_backward(const double* surfels, const SurfRec* recs, const int32_t* valid, int64_t n,
+                          const DevCamera& cam, const double* d_hinv, double* d_center, double* d_rot,
+                          double* d_scales, cudaStream_t st);
 
 // assign_labels (panoptic.cpp:36-91), labels.cu
 struct LabelParams {

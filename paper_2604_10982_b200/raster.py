@@ -371,6 +371,27 @@ class Renderer:
         _check(st, self.ctx, "render")
         return cnt if counters else None
 
+    def render_backward(self, scene, labels, cam: Camera, cfg: RasterConfig, g_color=None, g_sem=None,
+                        g_ins=None) -> dict:
+        """The render backward (pipeline.cpp:347-486) on the GPU: gradients of
+        L = <g_color, colour> + <g_sem, sem_feat> + <g_ins, ins_dist> w.r.t. every surfel parameter
+        (opacity, color, f_sem, labels, center, rotation, scales). `scene` is a SceneMap or a
+        DeviceScene (exact=True keeps the feature dot products in fp64)."""
+        lib = _lib.load()
+        ds = scene if isinstance(scene, DeviceScene) else DeviceScene(self, scene, labels, exact=True)
+        n = ds.n
+        gp = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in (g_color, g_sem, g_ins)]
+        out = {"opacity": np.zeros(n), "color": np.zeros((n, 3)), "f_sem": np.zeros((n, ds.c_sem)),
+               "labels": np.zeros((n, ds.n_q)), "center": np.zeros((n, 3)), "rotation": np.zeros((n, 4)),
+               "scales": np.zeros((n, 2))}
+        pg = A.psm_plane_grads(*[_ptr(a) for a in gp])
+        sg = A.psm_scene_grads(*[_ptr(out[k]) for k in ("opacity", "color", "f_sem", "labels", "center", "rotation",
+                                                          "scales")])
+        c_cam, c_cfg = cam.to_c(), cfg.to_c()
+        _check(lib.psm_render_backward(self.ctx, ds.handle, C.byref(c_cam), C.byref(c_cfg), C.byref(pg), C.byref(sg)),
+               self.ctx, "render_backward")
+        return out
+
     def sync(self) -> A.psm_counters:
         lib = _lib.load()
         _check(lib.psm_sync(self.ctx), self.ctx, "sync")
