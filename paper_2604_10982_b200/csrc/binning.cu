@@ -121,45 +121,114 @@ __device__ __forceinline__ uint64_t sort_key(uint64_t bits, uint32_t src, uint64
   return (((bits - min_bits) >> sh) << src_bits) | src;
 }
 
-__global__ void __launch_bounds__(256) emit_kernel(const int32_t* __restrict__ valid, int64_t n,
+// Warp-block masks in fp32 (the blend's 8 blocks of 8x4 pixels per tile; see
+// psm_block_mask for the fp64 statement). Conservative against fp32 rounding: k F11 and q
+// are inflated by 2e-4 relative (so the computed half-width squared never falls below the
+// true one, also at the ellipse's tips), each strip's y-range is widened by 0.1 px, and
+// the x-extent carries 0.05 px + 1e-5 of the magnitudes summed. Footprints with |centre|
+// or extent beyond 1e5 px keep every block.
+struct StripF {
+  float cx, cy, ymax, slope, dstar, kf11, q;
+};
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ bool strip_prep(const PsmEllipse& e, StripF* f) {
+  if (!e.ok || !(fabs(e.cx) < 1e5) || !(fabs(e.cy) < 1e5) || !(e.ymax < 1e5) || !(e.kf11 * e.q < 1e10)) return false;
+  f->cx = static_cast<float>(e.cx);
+  f->cy = static_cast<float>(e.cy);
+  f->kf11 = static_cast<float>(e.kf11 * 1.0002);
+  f->ymax = sqrtf(f->kf11);
+  f->slope = static_cast<float>(e.slope);
+  f->dstar = static_cast<float>(e.dstar);
+  f->q = static_cast<float>(e.q * 1.0002);
+  return true;
+}
+// Bit b of the result: block b of tile (tx, ty) may hold a pixel centre inside the ellipse.
+__device__ __forceinline__ void strips_f(const StripF& f, int ty, int height, float* sxl, float* sxr) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int y0 = ty * 16 + 4 * s;
+    const int y_end = min(y0 + 4, height);
+    const float dlo = fmaxf(static_cast<float>(y0) + 0.4f - f.cy, -f.ymax);
+    const float dhi = fminf(static_cast<float>(y_end) - 0.4f - f.cy, f.ymax);
+    const float dr = fminf(fmaxf(f.dstar, dlo), dhi);
+    const float dl = fminf(fmaxf(-f.dstar, dlo), dhi);
+    const float hr = sqrt_approx(fmaxf(f.kf11 - dr * dr, 0.f) * f.q);
+    const float hl = sqrt_approx(fmaxf(f.kf11 - dl * dl, 0.f) * f.q);
+    const float cr = f.cx + f.slope * dr, cl = f.cx + f.slope * dl;
+    const float mr = 0.05f + 1e-5f * (fabsf(f.cx) + fabsf(f.slope * dr) + hr);
+    const float ml = 0.05f + 1e-5f * (fabsf(f.cx) + fabsf(f.slope * dl) + hl);
+    const bool ok = y_end > y0 && dlo <= dhi + 1e-3f;
+    sxl[s] = ok ? cl - hl - ml : 3e38f;   // empty strip: [3e38, -3e38] meets nothing
+    sxr[s] = ok ? cr + hr + mr : -3e38f;
+  }
+}
+__device__ __forceinline__ uint32_t block_mask_f(const float* sxl, const float* sxr, int tx, int width) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int x0 = tx * 16 + 8 * h;
+    const int x_end = min(x0 + 8, width);
+    const float lo = static_cast<float>(x0) + 0.5f, hi = static_cast<float>(x_end) - 0.5f;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      if (x_end > x0 && sxl[s] <= hi && sxr[s] >= lo) m |= 1u << (2 * s + h);
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(256, 3) emit_kernel(const int32_t* __restrict__ valid, int64_t n,
                                                    const SurfRec* __restrict__ recs, const BinRec* __restrict__ bins,
                                                    DevRaster rs, int img_h, uint32_t* __restrict__ cursor,
                                                    const uint32_t* __restrict__ tile_start, uint32_t cap,
                                                    uint64_t* __restrict__ tile_keys,
                                                    const uint64_t* __restrict__ depth_bits,
-                                                   const unsigned long long* __restrict__ depth_minmax, int src_bits) {
+                                                   const unsigned long long* __restrict__ depth_minmax, int src_bits,
+                                                   int img_w) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n || !valid[i]) return;
-  const uint64_t key = sort_key(depth_bits[i], static_cast<uint32_t>(i), depth_minmax[0],
-                                key_shift(depth_minmax, src_bits), src_bits);
+  // the key's source field is (source << 8 | block mask), kFieldExtra bits wider than the source
+  const int fb = src_bits + kFieldExtra;
+  const uint64_t key = sort_key(depth_bits[i], static_cast<uint32_t>(i) << kFieldExtra, depth_minmax[0],
+                                key_shift(depth_minmax, fb), fb);
   const BinRec b = bins[i];
   if (b.tx0 > b.tx1 || b.ty0 > b.ty1) return;
   const bool ellipse = rs.binning == PSM_BIN_ELLIPSE;
+  // warp-block masks need the support cutoff (a pixel only uses candidates passing it)
+  const bool masks_on = rs.support_cutoff != 0;
   PsmEllipse e;
-  if (ellipse) e = psm_ellipse_prep(recs[i].cx, recs[i].cy, b.F00, b.F01, b.F11, rs.chi2);
+  if (ellipse || masks_on) e = psm_ellipse_prep(recs[i].cx, recs[i].cy, b.F00, b.F01, b.F11, rs.chi2);
+  StripF sf;
+  const bool strips = masks_on && strip_prep(e, &sf);
+  float sxl[4], sxr[4];
   uint32_t* cur = cursor + static_cast<int64_t>(threadIdx.x & (kSplit - 1)) * rs.tiles_x * rs.tiles_y;
   // tiles are claimed in batches of kBatch so several returning atomics are in flight at once
   constexpr int kBatch = 8;
-  int pend[kBatch];
+  uint32_t pend[kBatch];  // tile index | block mask << 24
   int np = 0;
   auto flush = [&]() {
     uint32_t o[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; ++u)
-      if (u < np) o[u] = atomicAdd(cur + pend[u], 1u);
+      if (u < np) o[u] = atomicAdd(cur + (pend[u] & 0xffffffu), 1u);
 #pragma unroll
     for (int u = 0; u < kBatch; ++u)
       if (u < np) {
-        const uint32_t at = __ldg(tile_start + pend[u]) + o[u];
-        if (at < cap) tile_keys[at] = key;
+        const uint32_t at = __ldg(tile_start + (pend[u] & 0xffffffu)) + o[u];
+        if (at < cap) tile_keys[at] = key | (pend[u] >> 24);
       }
     np = 0;
   };
   for (int ty = b.ty0; ty <= b.ty1; ++ty) {
     int lo = b.tx0, hi = b.tx1;
     if (ellipse && !psm_ellipse_row(e, ty, rs.tile_size, img_h, b.tx0, b.tx1, &lo, &hi)) continue;
+    if (strips) strips_f(sf, ty, img_h, sxl, sxr);
     for (int tx = lo; tx <= hi; ++tx) {
-      pend[np++] = ty * rs.tiles_x + tx;
+      const uint32_t bm = strips ? block_mask_f(sxl, sxr, tx, img_w) : 0xffu;
+      pend[np++] = static_cast<uint32_t>(ty * rs.tiles_x + tx) | bm << 24;
       if (np == kBatch) flush();
     }
   }
@@ -290,8 +359,8 @@ __device__ void merge_sort_regs(uint64_t (&v)[E], uint64_t* sm) {
 // truncated depth is insertion-sorted by the full key by the thread owning its first
 // entry, all runs in parallel. Repairing a run only permutes entries of equal truncated
 // depth, so concurrent readers of a run's border always see the same truncated key.
-__device__ void repair_truncated_runs(uint32_t* __restrict__ vals, int len, const uint64_t* __restrict__ depth_bits,
-                                      uint64_t dmin, int sh) {
+__device__ void repair_truncated_runs(uint32_t* __restrict__ vals, uint8_t* __restrict__ masks, int len,
+                                      const uint64_t* __restrict__ depth_bits, uint64_t dmin, int sh) {
   for (int i = threadIdx.x; i + 1 < len; i += blockDim.x) {
     const uint64_t ti = (depth_bits[vals[i]] - dmin) >> sh;
     if (i > 0 && ((depth_bits[vals[i - 1]] - dmin) >> sh) == ti) continue;  // not a run start
@@ -299,6 +368,7 @@ __device__ void repair_truncated_runs(uint32_t* __restrict__ vals, int len, cons
     while (j < len && ((depth_bits[vals[j]] - dmin) >> sh) == ti) ++j;
     for (int a = i + 1; a < j; ++a) {
       const uint32_t x = vals[a];
+      const uint8_t xm = masks[a];
       const uint64_t dx = depth_bits[x];
       int b = a - 1;
       while (b >= i) {
@@ -306,9 +376,11 @@ __device__ void repair_truncated_runs(uint32_t* __restrict__ vals, int len, cons
         const uint64_t dy = depth_bits[y];
         if (!(dy > dx || (dy == dx && y > x))) break;
         vals[b + 1] = y;
+        masks[b + 1] = masks[b];
         --b;
       }
       vals[b + 1] = x;
+      masks[b + 1] = xm;
     }
   }
 }
@@ -317,7 +389,8 @@ __device__ void repair_truncated_runs(uint32_t* __restrict__ vals, int len, cons
 // a truncated-key sort (sh > 0), runs of equal truncated depth are re-ordered by the
 // full (depth, source) order (rare).
 template <int NT, int E>
-__device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int start, int len,
+__device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint8_t* __restrict__ masks,
+                            int start, int len,
                             uint64_t* sm, const uint64_t* __restrict__ depth_bits, uint64_t dmin, int sh,
                             int src_bits) {
   uint64_t v[E];
@@ -335,7 +408,8 @@ __device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restr
   for (int e = 0; e < E; ++e) {
     const int i = threadIdx.x * E + e;
     if (i < len) {
-      vals[start + i] = static_cast<uint32_t>(v[e] & smask);
+      vals[start + i] = static_cast<uint32_t>((v[e] & smask) >> kFieldExtra);
+      masks[start + i] = static_cast<uint8_t>(v[e]);
       // neighbours with equal truncated depth: order unknown below the dropped bits
       if (sh > 0 && e + 1 < E && i + 1 < len && (v[e] >> src_bits) == (v[e + 1] >> src_bits)) bad = 1;
     }
@@ -346,7 +420,7 @@ __device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restr
     __syncthreads();
     if (threadIdx.x + 1 < NT && last + 1 < len && (v[E - 1] >> src_bits) == (sm[threadIdx.x + 1] >> src_bits)) bad = 1;
     __syncthreads();
-    if (bad) repair_truncated_runs(vals + start, len, depth_bits, dmin, sh);
+    if (bad) repair_truncated_runs(vals + start, masks + start, len, depth_bits, dmin, sh);
   }
 }
 
@@ -356,6 +430,7 @@ template <int NT, bool LARGE>
 __global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restrict__ ranges,
                                                         const uint64_t* __restrict__ keys,
                                                         uint32_t* __restrict__ tile_vals,
+                                                        uint8_t* __restrict__ tile_masks,
                                                         const uint64_t* __restrict__ depth_bits,
                                                         const unsigned long long* __restrict__ depth_minmax,
                                                         int src_bits) {
@@ -366,16 +441,24 @@ __global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restric
   const int sh = key_shift(depth_minmax, src_bits);
   const uint64_t dmin = depth_minmax[0];
   if (!LARGE) {
-    if (len <= 1 || len > 4096) return;
-    if (len <= 256) sort_bucket<NT, 2>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else if (len <= 512) sort_bucket<NT, 4>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else if (len <= 1024) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else if (len <= 2048) sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else sort_bucket<NT, 32>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
+    if (len < 1 || len > 4096) return;
+    if (len == 1) {  // nothing to sort: unpack the key
+      if (threadIdx.x == 0) {
+        const uint64_t v = keys[start];
+        tile_vals[start] = static_cast<uint32_t>((v & ((1ull << src_bits) - 1ull)) >> kFieldExtra);
+        tile_masks[start] = static_cast<uint8_t>(v);
+      }
+      return;
+    }
+    if (len <= 256) sort_bucket<NT, 2>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else if (len <= 512) sort_bucket<NT, 4>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else if (len <= 1024) sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else if (len <= 2048) sort_bucket<NT, 16>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else sort_bucket<NT, 32>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
   } else {
     if (len <= 4096 || len > 16384) return;
-    if (len <= 8192) sort_bucket<NT, 8>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else sort_bucket<NT, 16>(keys, tile_vals, start, len, sm, depth_bits, dmin, sh, src_bits);
+    if (len <= 8192) sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+    else sort_bucket<NT, 16>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
   }
 }
 
@@ -387,6 +470,7 @@ __global__ void __launch_bounds__(1024) sort_tiles_huge_kernel(const int32_t* __
                                                                uint64_t* __restrict__ keys,
                                                                uint64_t* __restrict__ scratch,
                                                                uint32_t* __restrict__ tile_vals,
+                                                               uint8_t* __restrict__ tile_masks,
                                                                const uint64_t* __restrict__ depth_bits,
                                                                const unsigned long long* __restrict__ depth_minmax,
                                                                int src_bits) {
@@ -449,11 +533,12 @@ __global__ void __launch_bounds__(1024) sort_tiles_huge_kernel(const int32_t* __
   if (threadIdx.x == 0) tie = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < len; i += NT) {
-    tile_vals[start + i] = static_cast<uint32_t>(src[i] & smask);
+    tile_vals[start + i] = static_cast<uint32_t>((src[i] & smask) >> kFieldExtra);
+    tile_masks[start + i] = static_cast<uint8_t>(src[i]);
     if (sh > 0 && i + 1 < len && (src[i] >> src_bits) == (src[i + 1] >> src_bits)) tie = 1;
   }
   __syncthreads();
-  if (tie) repair_truncated_runs(tile_vals + start, len, depth_bits, depth_minmax[0], sh);
+  if (tie) repair_truncated_runs(tile_vals + start, tile_masks + start, len, depth_bits, depth_minmax[0], sh);
 }
 
 __global__ void compact_kernel(const int32_t* __restrict__ valid, const int32_t* __restrict__ pos,
@@ -493,15 +578,16 @@ void launch_tile_scan(const uint32_t* tile_counts, int tiles, uint32_t cap, int3
 
 void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const BinRec* bins, const DevRaster& rs,
                  int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint64_t* tile_keys,
-                 const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, cudaStream_t st) {
+                 const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, int img_w,
+                 cudaStream_t st) {
   if (n > 0)
     emit_kernel<<<grid_for(n, 256), 256, 0, st>>>(valid, n, recs, bins, rs, img_h, cursor, tile_start, cap, tile_keys,
-                                                  depth_bits, depth_minmax, src_bits);
+                                                  depth_bits, depth_minmax, src_bits, img_w);
 }
 
 template <int NT, bool LARGE>
 void launch_sort_class(const int32_t* ranges, int tiles, const uint64_t* keys, uint32_t* tile_vals,
-                       const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
+                       uint8_t* tile_masks, const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
                        cudaStream_t st) {
   constexpr int smem = static_cast<int>(sizeof(uint64_t)) * (LARGE ? 16384 : 4096);
   static unsigned long long configured = 0;
@@ -511,18 +597,21 @@ void launch_sort_class(const int32_t* ranges, int tiles, const uint64_t* keys, u
     cudaFuncSetAttribute(sort_tiles_kernel<NT, LARGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured |= 1ull << dev;
   }
-  sort_tiles_kernel<NT, LARGE><<<tiles, NT, smem, st>>>(ranges, keys, tile_vals, depth_bits, depth_minmax, src_bits);
+  sort_tiles_kernel<NT, LARGE><<<tiles, NT, smem, st>>>(ranges, keys, tile_vals, tile_masks, depth_bits, depth_minmax,
+                                                        src_bits);
 }
 
 void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint64_t* key_scratch, uint32_t* tile_vals,
-                       const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
-                       cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
+                       uint8_t* tile_masks, const uint64_t* depth_bits, const unsigned long long* depth_minmax,
+                       int src_bits, cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
   if (tiles <= 0) return;
+  src_bits += kFieldExtra;  // the keys' source field carries the warp-block mask below the source
   // The few large buckets (one 1024-thread CTA per SM) run on a side stream, concurrently
   // with the many small ones, which fit beside them on every SM.
   cudaEventRecord(fork, st);
   cudaStreamWaitEvent(side, fork, 0);
-  launch_sort_class<1024, true>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, side);
+  launch_sort_class<1024, true>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits,
+                                side);
   {
     constexpr int smem = static_cast<int>(sizeof(uint64_t)) * kHugeChunk;
     static unsigned long long configured = 0;
@@ -532,10 +621,10 @@ void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, ui
       cudaFuncSetAttribute(sort_tiles_huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       configured |= 1ull << dev;
     }
-    sort_tiles_huge_kernel<<<tiles, 1024, smem, side>>>(ranges, tile_keys, key_scratch, tile_vals, depth_bits,
-                                                        depth_minmax, src_bits);
+    sort_tiles_huge_kernel<<<tiles, 1024, smem, side>>>(ranges, tile_keys, key_scratch, tile_vals, tile_masks,
+                                                        depth_bits, depth_minmax, src_bits);
   }
-  launch_sort_class<128, false>(ranges, tiles, tile_keys, tile_vals, depth_bits, depth_minmax, src_bits, st);
+  launch_sort_class<128, false>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, st);
   cudaEventRecord(join, side);
   cudaStreamWaitEvent(st, join, 0);
 }

@@ -26,6 +26,7 @@
 // accumulate VEC*NV channels each, then store the pixel's HWC channel run with
 // one coalesced vector store. Full blending with features keeps per-pixel
 // (source, weight) lists in an L2-resident global scratch.
+#include <algorithm>
 #include <cstdint>
 
 #include "psm_device.cuh"
@@ -77,7 +78,11 @@ __device__ unsigned long long psm_blend_stats[16];
 #endif
 
 constexpr size_t kExpTabBytes = 256 * sizeof(uint64_t);
-__host__ __device__ constexpr size_t stage_bytes(int kmax) { return static_cast<size_t>(kWarps) * 2 * chunk_for(kmax) * sizeof(SurfRec); }
+// per warp: [2][chunk] staged records + [2][chunk] their list positions (16 B aligned)
+__host__ __device__ constexpr size_t warp_stage_bytes(int kmax) {
+  return (2 * chunk_for(kmax) * (sizeof(SurfRec) + sizeof(int)) + 15) / 16 * 16;
+}
+__host__ __device__ constexpr size_t stage_bytes(int kmax) { return static_cast<size_t>(kWarps) * warp_stage_bytes(kmax); }
 __host__ __device__ constexpr size_t smem_bytes(int kmax) {
   return stage_bytes(kmax) + kExpTabBytes + static_cast<size_t>(kmax) * kThreads * (sizeof(double) + sizeof(int));
 }
@@ -134,63 +139,21 @@ __device__ __forceinline__ void accumulate_row(float (&acc)[NV][VEC], float w, c
   }
 }
 
-// Can the (inflated) support ellipse d^T Finv d <= chi2 of staged record r reach
-// any pixel centre of the warp's block [x0, x1] x [y0, y1] (already widened by the
-// absolute margin)? In F = Finv^-1 terms (Finv = [[a, b], [b, c]], D = ac - b^2):
-// half-height ey = sqrt(k a / D); over the strip dy in [y0 - cy, y1 - cy] the
-// ellipse's x-extent is slope*dy +- sqrt((k a / D - dy^2) D) / a with
-// slope = -b / a, the right edge maximised at dstar = -(b / D) sqrt(k D / c) clamped
-// into the strip (left edge at -dstar), as in psm_ellipse.h. fp32 with k inflated
-// by 1e-4 and a 0.02 px margin; ill-conditioned (D < 0.01 ac) or far-off-screen
-// footprints are always kept, so the per-pixel fp64 test (raster.cpp:379) never
-// passes where this says no.
-__device__ __forceinline__ bool cull_meets(const SurfRec& r, float k, float x0, float x1, float y0, float y1) {
-  const float a = static_cast<float>(r.f00), b = 0.5f * static_cast<float>(r.f01x2), c = static_cast<float>(r.f11);
-  const float cx = static_cast<float>(r.cx), cy = static_cast<float>(r.cy);
-  const float D = a * c - b * b;
-  if (!(D > 0.01f * a * c) || !(fabsf(cx) < 1e5f) || !(fabsf(cy) < 1e5f)) return true;
-  const float kf11 = k * a / D;
-  const float ey = sqrtf(kf11);
-  const float dlo = fmaxf(y0 - cy, -ey), dhi = fminf(y1 - cy, ey);
-  if (dlo > dhi) return false;
-  const float slope = -b / a;
-  const float dstar = -(b / D) * sqrtf(k * D / c);
-  const float dr = fminf(fmaxf(dstar, dlo), dhi);
-  const float dl = fminf(fmaxf(-dstar, dlo), dhi);
-  const float xr = cx + slope * dr + sqrtf(fmaxf(kf11 - dr * dr, 0.f) * D) / a;
-  const float xl = cx + slope * dl - sqrtf(fmaxf(kf11 - dl * dl, 0.f) * D) / a;
-  return xl <= x1 && xr >= x0;
-}
-
+// One warp's work item: the 8x4 pixel block `blk` (0..7) of tile `tile`; lane -> pixel.
 template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT, int PANO_T>
-__global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(BlendParams p) {
+__device__ __forceinline__ void blend_block(const BlendParams& p, const int tile, const int blk, SurfRec* stage,
+                                            const uint64_t* exp_tab, double* top_w, int* top_p) {
   constexpr int kChunk = chunk_for(KMAX);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  SurfRec* stage = reinterpret_cast<SurfRec*>(smem_raw) + (threadIdx.x >> 5) * 2 * kChunk;  // [2][kChunk]
-  // psm_exp's 2^(i/128) table, one copy per CTA (random per-lane lookups: shared memory, not L1)
-  uint64_t* exp_tab = reinterpret_cast<uint64_t*>(smem_raw + stage_bytes(KMAX));
-  // per-pixel Top-K lists (slot-major: [slot][thread], conflict-free): weights and list positions
-  double* top_w = reinterpret_cast<double*>(exp_tab + 256);
-  int* top_p = reinterpret_cast<int*>(top_w + KMAX * kThreads);
-  exp_tab[threadIdx.x] = psm_exp_tab_dev[threadIdx.x];
-  __syncthreads();
-
-  const int tile = p.tile_base + static_cast<int>(blockIdx.x);
   const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  // warp -> 8x4 block of the 16x16 tile; lane -> pixel inside it
-  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+  const int lane = tid & 31;
+  const int wx0 = tx * kTile + (blk & 1) * 8, wy0 = ty * kTile + (blk >> 1) * 4;
   const int x = wx0 + (lane & 7);
   const int y = wy0 + (lane >> 3);
   const bool inside = x < p.width && y < p.height;
   const int64_t pix = static_cast<int64_t>(y) * p.width + x;
 
   const double px = x + 0.5, py = y + 0.5;
-  // pixel-centre extents of the warp's 8x4 block (clipped to the image), widened by
-  // the prefilter's 0.02 px margin
-  const float bx0 = wx0 + 0.48f, by0 = wy0 + 0.48f;
-  const float bx1 = min(wx0 + 8, p.width) - 0.48f, by1 = min(wy0 + 4, p.height) - 0.48f;
   const double rx = (px - p.cam_cx) / p.cam_fx;  // division as in raster.cpp:370-371
   const double ry = (py - p.cam_cy) / p.cam_fy;
 
@@ -207,46 +170,78 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   int thr_p = 0;        // list position; never compared while thr_w < 0
 
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
-  const float kcull = static_cast<float>(p.chi2) * 1.0001f;
-  auto prefetch = [&](int base, int buf) {
-    if (lane < kChunk && base + lane < end) {
-      const int s = static_cast<int>(__ldg(p.vals + base + lane));
-      const char* g = reinterpret_cast<const char*>(p.recs + s);
-      char* d = reinterpret_cast<char*>(stage + buf * kChunk + lane);
+  int* spos = reinterpret_cast<int*>(stage + 2 * kChunk);  // [2][kChunk] list positions of the staged records
+  // The tile list is read in 32-entry windows (source id + warp-block mask per lane, the
+  // next window's loads in flight); the entries whose mask has this warp's block bit
+  // are compacted into chunks of kChunk staged records (cp.async by the owning lane).
+  const unsigned bbit = 1u << blk;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  int wb = start;
+  uint32_t cv = 0, nv = 0;
+  unsigned cm = 0, nm = 0;
+  if (start + lane < end) {
+    cv = __ldg(p.vals + start + lane);
+    cm = __ldg(p.masks + start + lane);
+  }
+  if (start + 32 + lane < end) {
+    nv = __ldg(p.vals + start + 32 + lane);
+    nm = __ldg(p.masks + start + 32 + lane);
+  }
+  unsigned clive = __ballot_sync(0xffffffffu, start + lane < end && (cm & bbit));
+  if (!p.support_cutoff) clive = __ballot_sync(0xffffffffu, start + lane < end);
+  // Stages the next (up to) kChunk live entries into buffer `bf`; returns how many.
+  auto assemble = [&](int bf) -> int {
+    int filled = 0;
+    for (;;) {
+      if (!clive) {
+        if (wb + 32 >= end) break;
+        wb += 32;
+        cv = nv;
+        cm = nm;
+        clive = __ballot_sync(0xffffffffu, wb + lane < end && (!p.support_cutoff || (cm & bbit)));
+        const int nxt = wb + 32 + lane;
+        if (nxt < end) {
+          nv = __ldg(p.vals + nxt);
+          nm = __ldg(p.masks + nxt);
+        }
+        continue;
+      }
+      const int r = __popc(clive & lt_mask);
+      const bool mine = (clive >> lane & 1u) && r < kChunk - filled;
+      const unsigned take = __ballot_sync(0xffffffffu, mine);
+      if (mine) {
+        const char* g = reinterpret_cast<const char*>(p.recs + cv);
+        char* d = reinterpret_cast<char*>(stage + bf * kChunk + filled + r);
 #pragma unroll
-      for (int k = 0; k < kRecVec; ++k) cp_async16(d + 16 * k, g + 16 * k);
+        for (int k = 0; k < kRecVec; ++k) cp_async16(d + 16 * k, g + 16 * k);
+        spos[bf * kChunk + filled + r] = wb + lane;
+      }
+      filled += __popc(take);
+      clive &= ~take;
+      if (filled == kChunk) break;
     }
     cp_async_commit();
+    return filled;
   };
 
 #ifdef PSM_BLEND_STATS
   unsigned st_iter = 0, st_sup = 0, st_alpha = 0, st_chunks = 0, st_streamed = 0, st_live = 0, st_any_sup = 0;
 #endif
-  if (__any_sync(0xffffffffu, !done) && start < end) prefetch(start, 0);
+  int cnt = __any_sync(0xffffffffu, !done) ? assemble(0) : 0;
   int buf = 0;
-  for (int base = start; base < end; base += kChunk, buf ^= 1) {
+  while (cnt > 0) {
     if (__all_sync(0xffffffffu, done)) break;
-    const int cnt = min(kChunk, end - base);
-    if (base + kChunk < end) {
-      prefetch(base + kChunk, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    const int ncnt = assemble(buf ^ 1);  // always commits one (possibly empty) group
+    cp_async_wait<1>();
     __syncwarp();
     const SurfRec* recs = stage + buf * kChunk;
-    // candidates that reach no pixel centre of this warp's block are skipped as a whole
-    unsigned live = (1u << cnt) - 1u;  // cnt <= 30
-    if (p.support_cutoff) live = __ballot_sync(0xffffffffu, lane < cnt && cull_meets(recs[lane], kcull, bx0, bx1, by0, by1));
 #ifdef PSM_BLEND_STATS
     st_chunks++;
-    st_streamed += cnt;
-    st_live += __popc(live);
+    st_live += cnt;
+    st_streamed = end - start;
 #endif
     if (!done) {
-      while (live) {
-        const int j = __ffs(live) - 1;
-        live &= live - 1;
+      for (int j = 0; j < cnt; ++j) {
         const SurfRec& r = recs[j];
 #ifdef PSM_BLEND_STATS
         st_iter++;
@@ -289,31 +284,33 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
           dom_w = wt;
           dom_depth = rcp;
         }
-        const int pos = base + j;  // list position; source id = vals[pos]
-        if constexpr (KMAX > 0) {
-          if (before(wt, pos, thr_w, thr_p, p.vals)) {  // insertion select (raster.cpp:238-249)
-            int i = n_top < klen ? n_top++ : klen - 1;  // the list fills without a threshold
-            while (i > 0) {
-              const double w = top_w[(i - 1) * kThreads + tid];
-              const int q = top_p[(i - 1) * kThreads + tid];
-              if (!before(wt, pos, w, q, p.vals)) break;
-              top_w[i * kThreads + tid] = w;
-              top_p[i * kThreads + tid] = q;
-              --i;
-            }
-            top_w[i * kThreads + tid] = wt;
-            top_p[i * kThreads + tid] = pos;
-            if (n_top == klen) {
-              thr_w = top_w[(klen - 1) * kThreads + tid];
-              thr_p = top_p[(klen - 1) * kThreads + tid];
+        if constexpr (KMAX > 0 || FULL_LIST) {
+          const int pos = spos[buf * kChunk + j];  // list position; source id = vals[pos]
+          if constexpr (KMAX > 0) {
+            if (before(wt, pos, thr_w, thr_p, p.vals)) {  // insertion select (raster.cpp:238-249)
+              int i = n_top < klen ? n_top++ : klen - 1;  // the list fills without a threshold
+              while (i > 0) {
+                const double w = top_w[(i - 1) * kThreads + tid];
+                const int q = top_p[(i - 1) * kThreads + tid];
+                if (!before(wt, pos, w, q, p.vals)) break;
+                top_w[i * kThreads + tid] = w;
+                top_p[i * kThreads + tid] = q;
+                --i;
+              }
+              top_w[i * kThreads + tid] = wt;
+              top_p[i * kThreads + tid] = pos;
+              if (n_top == klen) {
+                thr_w = top_w[(klen - 1) * kThreads + tid];
+                thr_p = top_p[(klen - 1) * kThreads + tid];
+              }
             }
           }
-        }
-        if constexpr (FULL_LIST) {
-          if (m < p.list_cap) {
-            p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(pos), __float_as_uint(wf));
-            if constexpr (PANO_T > 0) p.lists_w[pix * p.list_cap + m] = wt;
-            if (p.lists_t) p.lists_t[pix * p.list_cap + m] = T;  // backward cache: T before this blend
+          if constexpr (FULL_LIST) {
+            if (m < p.list_cap) {
+              p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(pos), __float_as_uint(wf));
+              if constexpr (PANO_T > 0) p.lists_w[pix * p.list_cap + m] = wt;
+              if (p.lists_t) p.lists_t[pix * p.list_cap + m] = T;  // backward cache: T before this blend
+            }
           }
         }
         T *= 1.0 - alpha;
@@ -324,7 +321,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
         }
       }
     }
-    __syncwarp();  // the buffer is refilled by the next iteration's prefetch
+    __syncwarp();  // the buffer is refilled by the next iteration's assemble
+    buf ^= 1;
+    cnt = ncnt;
   }
   cp_async_wait<0>();
 #ifdef PSM_BLEND_STATS
@@ -584,6 +583,35 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
   }
 }
 
+// Persistent CTAs (resident count per SM x SMs): each warp pulls (tile, 8x4 block) items
+// from the launch's work counter until the tiles run out, so an SM's slots are never held
+// by a CTA whose other warps already finished (tile depth complexity varies 10x+ across
+// a frame). A warp's shared memory (staging, Top-K columns) is private to it; the exp
+// table is loaded once per CTA.
+template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT, int PANO_T>
+__global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(BlendParams p) {
+  constexpr int kChunk = chunk_for(KMAX);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SurfRec* stage = reinterpret_cast<SurfRec*>(smem_raw + (threadIdx.x >> 5) * warp_stage_bytes(KMAX));  // [2][kChunk]
+  // psm_exp's 2^(i/128) table, one copy per CTA (random per-lane lookups: shared memory, not L1)
+  uint64_t* exp_tab = reinterpret_cast<uint64_t*>(smem_raw + stage_bytes(KMAX));
+  // per-pixel Top-K lists (slot-major: [slot][thread], conflict-free): weights and list positions
+  double* top_w = reinterpret_cast<double*>(exp_tab + 256);
+  int* top_p = reinterpret_cast<int*>(top_w + KMAX * kThreads);
+  exp_tab[threadIdx.x] = psm_exp_tab_dev[threadIdx.x];
+  __syncthreads();
+  const int n_items = p.n_tiles * kWarps;
+  for (;;) {
+    int item = 0;
+    if ((threadIdx.x & 31) == 0) item = atomicAdd(p.work, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    blend_block<KMAX, FULL_LIST, VEC, NV, LPP, EXACT, PANO_T>(p, p.tile_base + item / kWarps, item % kWarps, stage,
+                                                              exp_tab, top_w, top_p);
+    __syncwarp();  // the lanes' Top-K columns and staging are rewritten by the next item
+  }
+}
+
 template <int KMAX, bool FULL, int VEC, int NV, int LPP, bool EXACT, int PANO_T = 0>
 void launch_t(const BlendParams& p, int tiles, cudaStream_t st) {
   auto kern = blend_kernel<KMAX, FULL, VEC, NV, LPP, EXACT, PANO_T>;
@@ -594,7 +622,12 @@ void launch_t(const BlendParams& p, int tiles, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_bytes(KMAX)));
     configured |= 1ull << dev;
   }
-  kern<<<tiles, kThreads, smem_bytes(KMAX), st>>>(p);
+  static int sms[64] = {};
+  if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::min(tiles, sms[dev] * min_blocks(KMAX));
+  BlendParams q = p;
+  q.n_tiles = tiles;
+  kern<<<grid, kThreads, smem_bytes(KMAX), st>>>(q);
 }
 
 // Feature-lane shapes: float4 lanes, 32/LPP pixels per warp iteration for the

@@ -73,7 +73,7 @@ struct psm_ctx {
   psm::Buf recs, bins, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, kscratch2, valid, pos, keys_c, src_c, keys_s, src_s;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
   psm::Buf lists_w, pan_ids, pan_classes, pan_sem, qclass, lab_tmp, lab_scratch, lab_dist, lab_arg;
-  psm::Buf lists_t, topk_pos, bw_gin, bw_out;
+  psm::Buf lists_t, topk_pos, bw_gin, bw_out, tmasks;
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
   psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
@@ -203,12 +203,12 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   // device counters (8-byte slots): [0] err, [1] nonempty tiles, [2] blended_total, [3] list overflow,
   // [4] n_proj (u32), [5] RN-Total (u32), [6] RN kept (u32), [7] key overflow
   unsigned long long* small = nullptr;
-  PSM_TRY(ensure(ctx, ctx->dev_small, 8, &small));
+  PSM_TRY(ensure(ctx, ctx->dev_small, 16, &small));  // [8, 16): blend work counters
   uint32_t* n_proj_dev = reinterpret_cast<uint32_t*>(small + 4);
   uint32_t* rn_dev = reinterpret_cast<uint32_t*>(small + 5);
   uint32_t* rn_eff_dev = reinterpret_cast<uint32_t*>(small + 6);
   int32_t* key_ovf = reinterpret_cast<int32_t*>(small + 7);
-  PSM_CUDA_TRY(cudaMemsetAsync(small, 0, 8 * sizeof(unsigned long long), st));
+  PSM_CUDA_TRY(cudaMemsetAsync(small, 0, 16 * sizeof(unsigned long long), st));
   int32_t* ranges = nullptr;
   PSM_TRY(ensure(ctx, ctx->ranges, static_cast<size_t>(tiles) * 2, &ranges));
   PSM_CUDA_TRY(cudaMemsetAsync(ranges, 0, sizeof(int32_t) * 2 * tiles, st));
@@ -216,6 +216,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   ctx->ev_next = 0;
   record(ctx, 0);
   uint32_t* tvals_s = nullptr;
+  uint8_t* tmasks_s = nullptr;
   int64_t key_cap = 0;
   if (n > 0) {
     SurfRec* recs; BinRec* bins; uint64_t* dbits; int32_t* valid;
@@ -251,8 +252,10 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     key_cap = ctx->key_cap;
     if (key_cap > 0x7fffffffLL) return fail(ctx, PSM_EUNSUPPORTED, "RN-Total exceeds 2^31 tile assignments");
     uint32_t* tvals;
+    uint8_t* tmasks;
     uint64_t *tkeys, *tkeys2;
     PSM_TRY(ensure(ctx, ctx->tvals, key_cap, &tvals));
+    PSM_TRY(ensure(ctx, ctx->tmasks, key_cap, &tmasks));
     PSM_TRY(ensure(ctx, ctx->kscratch, key_cap, &tkeys));
     PSM_TRY(ensure(ctx, ctx->kscratch2, key_cap, &tkeys2));
     int src_bits = 1;
@@ -265,14 +268,15 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     record(ctx, 2);
     // K4: every (surfel, tile) pair into its tile's bucket
     launch_emit(valid, n, recs, bins, rs, H, cursor, tstart, static_cast<uint32_t>(key_cap), tkeys, dbits, dminmax,
-                src_bits, st);
+                src_bits, W, st);
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 3);
     // K5: per-tile sort by (depth bits, source)
-    launch_sort_tiles(ranges, tiles, tkeys, tkeys2, tvals, dbits, dminmax, src_bits, st, ctx->side, ctx->fork,
+    launch_sort_tiles(ranges, tiles, tkeys, tkeys2, tvals, tmasks, dbits, dminmax, src_bits, st, ctx->side, ctx->fork,
                       ctx->join);
     PSM_CUDA_TRY(cudaGetLastError());
     tvals_s = tvals;
+    tmasks_s = tmasks;
     record(ctx, 4);
   }
   // K7: blend
@@ -280,6 +284,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   std::memset(&bp, 0, sizeof bp);
   bp.ranges = ranges;
   bp.vals = tvals_s;
+  bp.masks = tmasks_s;
   bp.recs = static_cast<const SurfRec*>(ctx->recs.p);
   bp.feat = sc->feat;
   bp.feat_dims = feat_dims; bp.c_sem = sc->c_sem; bp.n_q = sc->n_q;
@@ -332,6 +337,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     bp.n_query_class = pl.n_qclass;
   }
   if (!on_band) {
+    bp.work = reinterpret_cast<int32_t*>(small + 8);
     launch_blend(bp, tiles, topk, st);
     PSM_CUDA_TRY(cudaGetLastError());
   } else {
@@ -339,6 +345,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     for (int b = 0; b < bands; ++b) {
       const int ty0 = tiles_y * b / bands, ty1 = tiles_y * (b + 1) / bands;
       bp.tile_base = ty0 * tiles_x;
+      bp.work = reinterpret_cast<int32_t*>(small + 8 + b);
       launch_blend(bp, (ty1 - ty0) * tiles_x, topk, st);
       PSM_CUDA_TRY(cudaGetLastError());
       PSM_TRY((*on_band)(b, ty0 * ts, ty1 * ts < H ? ty1 * ts : H));
@@ -627,7 +634,7 @@ int psm_destroy(psm_ctx* ctx) {
   psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->depth_bits, &ctx->dminmax, &ctx->tile_counts, &ctx->cursor, &ctx->tile_totals, &ctx->tile_start, &ctx->kscratch, &ctx->kscratch2, &ctx->valid, &ctx->pos,
                       &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s,
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
-                      &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg,
+                      &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg, &ctx->tmasks,
                       &ctx->lists_w, &ctx->pan_ids, &ctx->pan_classes, &ctx->pan_sem, &ctx->qclass, &ctx->lab_tmp,
                       &ctx->lab_scratch, &ctx->lab_dist, &ctx->lab_arg, &ctx->lists_t, &ctx->topk_pos, &ctx->bw_gin,
                       &ctx->bw_out,

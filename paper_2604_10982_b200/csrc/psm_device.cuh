@@ -38,6 +38,9 @@ static_assert(sizeof(BinRec) == 48, "BinRec must be 48 bytes");
 
 // Sub-buckets per tile for the counting sort's atomics (binning.cu).
 constexpr int kSplit = 32;
+// Bits below the source id in a tile sort key: the 8-bit warp-block live mask of the
+// (surfel, tile) entry (psm_block_mask), carried through the sort beside the source.
+constexpr int kFieldExtra = 8;
 
 // Camera by value in kernel parameters.
 struct DevCamera {

@@ -59,19 +59,10 @@ PSM_EHD PsmEllipse psm_ellipse_prep(double cx, double cy, double f00, double f01
   return e;
 }
 
-// Tile-column run [*tx_lo, *tx_hi] of tile row `ty` met by the ellipse, intersected
-// with the AABB columns [ax0, ax1]. Returns 0 if the row is empty.
-PSM_EHD int psm_ellipse_row(const PsmEllipse& e, int ty, int ts, int height, int ax0, int ax1, int* tx_lo,
-                            int* tx_hi) {
-  if (!e.ok) {  // degenerate / ill-conditioned: keep the AABB row
-    *tx_lo = ax0;
-    *tx_hi = ax1;
-    return ax0 <= ax1;
-  }
-  const double y_lo = ty * ts + 0.5;
-  int y_end = ty * ts + ts;
-  if (y_end > height) y_end = height;
-  const double y_hi = y_end - 0.5;
+// x-extent [*xl, *xr] (with the 1e-3 px margin) of the ellipse over the rows of pixel
+// centres y in [y_lo, y_hi]. Returns 0 if the strip misses the ellipse's y-extent.
+// Requires e.ok.
+PSM_EHD int psm_ellipse_span(const PsmEllipse& e, double y_lo, double y_hi, double* xl, double* xr) {
   double dlo = y_lo - e.cy;
   double dhi = y_hi - e.cy;
   if (dlo < -e.ymax) dlo = -e.ymax;
@@ -87,8 +78,26 @@ PSM_EHD int psm_ellipse_row(const PsmEllipse& e, int ty, int ts, int height, int
   double rl = e.kf11 - dl * dl;
   if (rr < 0.0) rr = 0.0;
   if (rl < 0.0) rl = 0.0;
-  const double xr = e.cx + e.slope * dr + sqrt(rr * e.q) + 1e-3;
-  const double xl = e.cx + e.slope * dl - sqrt(rl * e.q) - 1e-3;
+  *xr = e.cx + e.slope * dr + sqrt(rr * e.q) + 1e-3;
+  *xl = e.cx + e.slope * dl - sqrt(rl * e.q) - 1e-3;
+  return 1;
+}
+
+// Tile-column run [*tx_lo, *tx_hi] of tile row `ty` met by the ellipse, intersected
+// with the AABB columns [ax0, ax1]. Returns 0 if the row is empty.
+PSM_EHD int psm_ellipse_row(const PsmEllipse& e, int ty, int ts, int height, int ax0, int ax1, int* tx_lo,
+                            int* tx_hi) {
+  if (!e.ok) {  // degenerate / ill-conditioned: keep the AABB row
+    *tx_lo = ax0;
+    *tx_hi = ax1;
+    return ax0 <= ax1;
+  }
+  const double y_lo = ty * ts + 0.5;
+  int y_end = ty * ts + ts;
+  if (y_end > height) y_end = height;
+  const double y_hi = y_end - 0.5;
+  double xl, xr;
+  if (!psm_ellipse_span(e, y_lo, y_hi, &xl, &xr)) return 0;
   // tiles whose pixel-centre span [tx*ts + 0.5, tx*ts + ts - 0.5] meets [xl, xr]
   double lo = ceil(psm_div_tile(xl - (ts - 0.5), ts));
   double hi = floor(psm_div_tile(xr - 0.5, ts));

@@ -12,11 +12,14 @@ namespace psm {
 struct BlendParams {
   const int32_t* ranges;  // [tiles][2]
   const uint32_t* vals;   // tile-sorted source ids
+  const uint8_t* masks;   // beside vals: warp-block live masks (bit b: block b may be reached)
   const SurfRec* recs;
   const float* feat;      // [N][feat_dims]: f_sem | labels, fp32
   int32_t feat_dims, c_sem, n_q;
   int32_t width, height, tiles_x;
-  int32_t tile_base;      // first tile of this launch (row bands: blockIdx.x + tile_base)
+  int32_t tile_base;      // first tile of this launch (row bands)
+  int32_t n_tiles;        // tiles of this launch (set by launch_blend)
+  int32_t* work;          // zeroed work counter of this launch: (tile, 8x4 block) items taken
   double cam_cx, cam_cy, cam_fx, cam_fy;
   double chi2, alpha_min, t_min, bg0, bg1, bg2;
   int32_t support_cutoff, render_depth_normal, k_sel;
@@ -92,10 +95,11 @@ void launch_tile_scan(const uint32_t* tile_counts, int tiles, uint32_t cap, int3
                       unsigned long long* nonempty, int32_t* overflow, cudaStream_t st);
 void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const BinRec* bins, const DevRaster& rs,
                  int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint64_t* tile_keys,
-                 const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, cudaStream_t st);
+                 const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, int img_w,
+                 cudaStream_t st);
 void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint64_t* key_scratch, uint32_t* tile_vals,
-                       const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
-                       cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
+                       uint8_t* tile_masks, const uint64_t* depth_bits, const unsigned long long* depth_minmax,
+                       int src_bits, cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n,
                     uint64_t* keys_out, uint32_t* src_out, cudaStream_t st);
 void launch_rank_of(const uint32_t* src_by_rank, const uint32_t* n_proj_dev, int64_t cap, int32_t* rank_of,

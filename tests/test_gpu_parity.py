@@ -95,6 +95,21 @@ def test_gpu_single_opaque_surfel(rend):
     assert abs(g.depth[y, x, 0] - 2.0) < 1e-5 and abs(g.depth[y, x, 1] - 2.0) < 1e-5
 
 
+def test_gpu_single_entry_tiles_after_dense_frame(rend):
+    """Tiles holding exactly one (surfel, tile) entry (no sort needed) must still get that entry's
+    source id and warp-block mask, also when the context's buffers hold a previous frame's lists."""
+    sc, _, cam = make_street_scene(StreetSpec(n_surfels=3000, image_w=128, image_h=96, c_sem=0), with_labels=False)
+    assert_parity(rend, sc, None, cam, RasterConfig())  # fills the key/list buffers with other data
+    cam = front_camera(128, 96)
+    # small surfels far apart (each alone in its tiles), placed so that their ids are non-zero
+    far = [facing_surfel((0, 0, -5), 0.2, 0.2, 1.0, (1, 1, 1))] * 3  # culled (behind the camera)
+    iso = [facing_surfel((dx, dy, 4), 0.05, 0.05, 0.9, (0.2 + 0.1 * i, 0.5, 0.7))
+           for i, (dx, dy) in enumerate([(-1.5, -1.0), (0.0, 0.0), (1.6, 1.1), (1.5, -1.2)])]
+    for binning in (Binning.Circle, Binning.Aabb, Binning.Ellipse):
+        g, _ = assert_parity(rend, scene_of(far + iso), None, cam, RasterConfig(binning=binning))
+        assert np.count_nonzero(g.blend_count) > 0
+
+
 def test_gpu_two_surfel_alpha_arithmetic(rend):
     cam = front_camera()
     sc = scene_of([facing_surfel((0, 0, 2), 0.2, 0.2, 0.5, (1, 0, 0)),
