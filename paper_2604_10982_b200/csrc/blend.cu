@@ -47,10 +47,10 @@ constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
 // chunk is the largest that fits the residency (228 KB per SM, 1 KB reserved per
 // CTA) and the registers stay under 65536 / (256 x blocks).
 #ifndef PSM_BLEND_CH8
-#define PSM_BLEND_CH8 12
+#define PSM_BLEND_CH8 16
 #endif
 #ifndef PSM_BLEND_MB8
-#define PSM_BLEND_MB8 4
+#define PSM_BLEND_MB8 3
 #endif
 #ifndef PSM_BLEND_CH16
 #define PSM_BLEND_CH16 10
@@ -240,33 +240,60 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     st_live += cnt;
     st_streamed = end - start;
 #endif
+    // Support phase (raster.cpp:375-382): bit j of `sup` = staged entry j passes this
+    // pixel's support test; `need` = the entries some pixel of the warp needs.
+    unsigned sup = 0;
     if (!done) {
-      for (int j = 0; j < cnt; ++j) {
-        const SurfRec& r = recs[j];
-#ifdef PSM_BLEND_STATS
-        st_iter++;
-        {
-          const double dx = px - r.cx, dy = py - r.cy;
-          const bool sp = !p.support_cutoff || !(r.f00 * dx * dx + r.f01x2 * dx * dy + r.f11 * dy * dy > p.chi2);
-          const unsigned am = __activemask();
-          const unsigned bm = __ballot_sync(am, sp);
-          if (sp) st_sup++;
-          if (lane == __ffs(am) - 1 && bm) st_any_sup++;
-        }
-#endif
-        if (p.support_cutoff) {
+      if (p.support_cutoff) {
+        for (int j = 0; j < cnt; ++j) {
+          const SurfRec& r = recs[j];
           const double dx = px - r.cx;
           const double dy = py - r.cy;
-          if (r.f00 * dx * dx + r.f01x2 * dx * dy + r.f11 * dy * dy > p.chi2) continue;  // raster.cpp:379
+          if (!(r.f00 * dx * dx + r.f01x2 * dx * dy + r.f11 * dy * dy > p.chi2)) sup |= 1u << j;  // raster.cpp:379
         }
-        const double w0 = r.h[0] * rx + r.h[1] * ry + r.h[2];
-        const double w1 = r.h[3] * rx + r.h[4] * ry + r.h[5];
-        const double w2 = r.h[6] * rx + r.h[7] * ry + r.h[8];
-        if (!(w2 > 1e-14)) continue;
-        const double rcp = 1.0 / w2;
-        const double u = w0 * rcp, v = w1 * rcp;
-        const double alpha = r.opacity * psm_exp_t(-0.5 * (u * u + v * v), exp_tab);
-        if (alpha < p.alpha_min || alpha <= 0.0) continue;
+      } else {
+        sup = cnt >= 32 ? 0xffffffffu : (1u << cnt) - 1u;
+      }
+    }
+    unsigned need = __reduce_or_sync(0xffffffffu, sup);
+#ifdef PSM_BLEND_STATS
+    st_sup += __popc(sup);
+    st_iter += __popc(need);
+#endif
+    // Alpha phase: the needed entries two at a time (two independent homography /
+    // division / exp chains in flight), then composited in list order.
+    while (need) {
+      const int j0 = __ffs(need) - 1;
+      need &= need - 1;
+      const int j1 = need ? __ffs(need) - 1 : j0;
+      need &= need - 1;
+      const SurfRec& r0 = recs[j0];
+      const SurfRec& r1 = recs[j1];
+      const double w00 = r0.h[0] * rx + r0.h[1] * ry + r0.h[2];
+      const double w01 = r0.h[3] * rx + r0.h[4] * ry + r0.h[5];
+      const double w02 = r0.h[6] * rx + r0.h[7] * ry + r0.h[8];
+      const double w10 = r1.h[0] * rx + r1.h[1] * ry + r1.h[2];
+      const double w11 = r1.h[3] * rx + r1.h[4] * ry + r1.h[5];
+      const double w12 = r1.h[6] * rx + r1.h[7] * ry + r1.h[8];
+      const double rcp0 = 1.0 / w02, rcp1 = 1.0 / w12;
+      const double u0 = w00 * rcp0, v0 = w01 * rcp0;
+      const double u1 = w10 * rcp1, v1 = w11 * rcp1;
+      const double x0 = -0.5 * (u0 * u0 + v0 * v0), x1 = -0.5 * (u1 * u1 + v1 * v1);
+      double e0 = psm_exp_main(x0, exp_tab), e1 = psm_exp_main(x1, exp_tab);
+      if (!psm_exp_main_ok(x0)) e0 = psm_exp_t(x0, exp_tab);
+      if (!psm_exp_main_ok(x1)) e1 = psm_exp_t(x1, exp_tab);
+      const double a0 = r0.opacity * e0, a1 = r1.opacity * e1;
+      // (w2 > 1e-14, raster.cpp:386-387; alpha >= alpha_min and > 0, :391)
+      bool ok[2];
+      ok[0] = !done && (sup >> j0 & 1u) && (w02 > 1e-14) && !(a0 < p.alpha_min || a0 <= 0.0);
+      ok[1] = !done && j1 != j0 && (sup >> j1 & 1u) && (w12 > 1e-14) && !(a1 < p.alpha_min || a1 <= 0.0);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (!ok[c] || done) continue;
+        const SurfRec& r = c ? r1 : r0;
+        const double alpha = c ? a1 : a0;
+        const double rcp = c ? rcp1 : rcp0;
+        const int j = c ? j1 : j0;
 #ifdef PSM_BLEND_STATS
         st_alpha++;
 #endif
@@ -315,11 +342,9 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         }
         T *= 1.0 - alpha;
         ++m;
-        if (T < p.t_min) {
-          done = true;
-          break;
-        }
+        if (T < p.t_min) done = true;
       }
+      if (__all_sync(0xffffffffu, done)) break;
     }
     __syncwarp();  // the buffer is refilled by the next iteration's assemble
     buf ^= 1;

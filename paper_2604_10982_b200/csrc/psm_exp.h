@@ -161,6 +161,36 @@ PSM_HD double psm_exp_t(double x, const uint64_t* tab) {
   return psm_fma(scale, tmp, scale);
 }
 
+// The common case of psm_exp_t (2^-54 <= |x| < 512) without its range branches, so
+// that two independent evaluations can be interleaved; psm_exp_t(x) == psm_exp_main(x)
+// whenever psm_exp_main_ok(x).
+PSM_HD bool psm_exp_main_ok(double x) {
+  const uint32_t abstop = static_cast<uint32_t>(psm_double_to_bits(x) >> 52) & 0x7ffu;
+  return abstop - 0x3c9u < 0x3fu;
+}
+PSM_HD double psm_exp_main(double x, const uint64_t* tab) {
+  const double kInvLn2N = PSM_EXPK(0, 0x1.71547652b82fep7);
+  const double kShift = 0x1.8p52;
+  const double kNegLn2HiN = PSM_EXPK(2, -0x1.62e42fefa0000p-8);
+  const double kNegLn2LoN = PSM_EXPK(3, -0x1.cf79abc9e3b3ap-47);
+  const double C2 = PSM_EXPK(4, 0x1.ffffffffffdbdp-2), C3 = PSM_EXPK(5, 0x1.555555555543cp-3);
+  const double C4 = PSM_EXPK(6, 0x1.55555cf172b91p-5), C5 = PSM_EXPK(7, 0x1.1111167a4d017p-7);
+  double kd = psm_fma(x, kInvLn2N, kShift);
+  const uint64_t ki = psm_double_to_bits(kd);
+  kd = kd - kShift;
+  double r = psm_fma(kd, kNegLn2HiN, x);
+  r = psm_fma(kd, kNegLn2LoN, r);
+  double tail;
+  uint64_t sbits;
+  psm_exp_tab(tab, 2 * (ki % 128), &tail, &sbits);
+  sbits += ki << 45;
+  const double r2 = r * r;
+  const double t1 = psm_fma(psm_fma(r, C3, C2), r2, r + tail);
+  const double tmp = psm_fma(r2 * r2, psm_fma(r, C5, C4), t1);
+  const double scale = psm_bits_to_double(sbits);
+  return psm_fma(scale, tmp, scale);
+}
+
 PSM_HD double psm_exp(double x) {
 #if defined(__CUDA_ARCH__)
   return psm_exp_t(x, psm_exp_tab_dev);
