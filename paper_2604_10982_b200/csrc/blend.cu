@@ -437,15 +437,13 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       if constexpr (KMAX > 0) {
         const int qt = (tid & ~31) + q;  // the pixel's thread: its Top-K list column
         for (int i = 0; i < nq; ++i) {
-          {
-            const int s = static_cast<int>(__ldg(p.vals + top_p[i * kThreads + qt]));
-            const float w = static_cast<float>(top_w[i * kThreads + qt]);
-            const TV* row = reinterpret_cast<const TV*>(p.feat + static_cast<int64_t>(s) * D);
+          const int s = static_cast<int>(__ldg(p.vals + top_p[i * kThreads + qt]));
+          const float w = static_cast<float>(top_w[i * kThreads + qt]);
+          const TV* row = reinterpret_cast<const TV*>(p.feat + static_cast<int64_t>(s) * D);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-              const int idx = v * LPP + sub;
-              if (EXACT || idx * VEC < D) fma_vec<VEC>(acc[v], w, __ldg(row + idx));
-            }
+          for (int v = 0; v < NV; ++v) {
+            const int idx = v * LPP + sub;
+            if (EXACT || idx * VEC < D) fma_vec<VEC>(acc[v], w, __ldg(row + idx));
           }
         }
       } else {
@@ -557,23 +555,44 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       double acc[PANO_T];
 #pragma unroll
       for (int t = 0; t < PANO_T; ++t) acc[t] = 0.0;
-      for (int i = 0; i < (D > 0 ? nq : 0); ++i) {
-        int pos;
-        double w;
-        if constexpr (KMAX > 0) {
-          pos = top_p[i * kThreads + (tid & ~31) + q];
-          w = top_w[i * kThreads + (tid & ~31) + q];
-        } else {
-          pos = static_cast<int>(p.lists[qpix * p.list_cap + i].x);
-          w = p.lists_w[qpix * p.list_cap + i];
+      if constexpr (KMAX > 0) {
+        // lane i < nq fetches slot i's source and weight; the rows are then loaded back to
+        // back and summed in blend order
+        const int i_l = lane < KMAX ? lane : 0;
+        int src = 0;
+        double sw = 0.0;
+        if (lane < nq && D > 0) {
+          src = static_cast<int>(__ldg(p.vals + top_p[i_l * kThreads + (tid & ~31) + q]));
+          sw = top_w[i_l * kThreads + (tid & ~31) + q];
         }
-        const double* row = p.feat64 + static_cast<int64_t>(__ldg(p.vals + pos)) * D;
 #pragma unroll
-        for (int t = 0; t < PANO_T; ++t) {
-          const int c = lane + 32 * t;
-          if (c < D) {
-            const double v = __ldg(row + c);
-            acc[t] = i == 0 ? w * v : acc[t] + w * v;
+        for (int i = 0; i < KMAX; ++i) {
+          const int s_i = __shfl_sync(0xffffffffu, src, i);
+          const double w = __shfl_sync(0xffffffffu, sw, i);
+          if (i < nq && D > 0) {
+            const double* row = p.feat64 + static_cast<int64_t>(s_i) * D;
+#pragma unroll
+            for (int t = 0; t < PANO_T; ++t) {
+              const int c = lane + 32 * t;
+              if (c < D) {
+                const double v = __ldg(row + c);
+                acc[t] = i == 0 ? w * v : acc[t] + w * v;
+              }
+            }
+          }
+        }
+      } else {
+        for (int i = 0; i < (D > 0 ? nq : 0); ++i) {
+          const int pos = static_cast<int>(p.lists[qpix * p.list_cap + i].x);
+          const double w = p.lists_w[qpix * p.list_cap + i];
+          const double* row = p.feat64 + static_cast<int64_t>(__ldg(p.vals + pos)) * D;
+#pragma unroll
+          for (int t = 0; t < PANO_T; ++t) {
+            const int c = lane + 32 * t;
+            if (c < D) {
+              const double v = __ldg(row + c);
+              acc[t] = i == 0 ? w * v : acc[t] + w * v;
+            }
           }
         }
       }
