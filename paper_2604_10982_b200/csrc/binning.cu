@@ -17,6 +17,9 @@
 //                  <= 16384 (1024 threads), larger by a bitonic network over global memory.
 // Every count stays on the device; key buffers are capacity-checked (the host
 // re-renders a frame whose RN-Total outgrew them, capi.cu).
+#include <algorithm>
+#include <cstdint>
+
 #include "psm_device.cuh"
 #include "psm_ellipse.h"
 #include "psm_kernels.h"
@@ -45,14 +48,30 @@ __global__ void __launch_bounds__(256) tile_sub_scan_kernel(const uint32_t* __re
   totals[t] = run;
 }
 
+// Per-tile sort size classes (K5): 0: 1..4096 keys (128 threads), 1: ..8192 and
+// 2: ..16384 (1024 threads, 64 / 128 KB of shared memory), 3: beyond (chunked + global
+// merge passes). K3b lists each class's tiles: classes[c * tiles + i], count at
+// classes[kSortClasses * tiles + c].
+constexpr int kSortClasses = 4;
+__device__ __forceinline__ int sort_class(int len) {
+  if (len < 1) return -1;
+  if (len <= 4096) return 0;
+  if (len <= 8192) return 1;
+  if (len <= 16384) return 2;
+  return 3;
+}
+
 // K3b: one CTA scans the tile totals: ranges, tile starts, RN-Total, non-empty tiles.
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ totals, int tiles, uint32_t cap,
                                                         int32_t* __restrict__ ranges, uint32_t* __restrict__ tile_start,
                                                         uint32_t* __restrict__ rn_dev, uint32_t* __restrict__ rn_eff,
                                                         unsigned long long* __restrict__ nonempty,
-                                                        int32_t* __restrict__ overflow) {
+                                                        int32_t* __restrict__ overflow,
+                                                        int32_t* __restrict__ classes) {
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t warp_ne[32];
+  __shared__ int cls_n[kSortClasses];
+  if (threadIdx.x < kSortClasses) cls_n[threadIdx.x] = 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int per = (tiles + 1023) / 1024;  // consecutive tiles per thread
   const int t0 = tid * per;
@@ -90,11 +109,16 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     if (t < tiles) {
       const uint32_t v = totals[t];
       tile_start[t] = run;
-      ranges[2 * t] = static_cast<int32_t>(min(run, cap));
-      ranges[2 * t + 1] = static_cast<int32_t>(min(run + v, cap));
+      const uint32_t b = min(run, cap), e = min(run + v, cap);
+      ranges[2 * t] = static_cast<int32_t>(b);
+      ranges[2 * t + 1] = static_cast<int32_t>(e);
       run += v;
+      const int c = sort_class(static_cast<int>(e - b));
+      if (c >= 0) classes[c * tiles + atomicAdd(&cls_n[c], 1)] = t;
     }
   }
+  __syncthreads();
+  if (tid < kSortClasses) classes[kSortClasses * tiles + tid] = cls_n[tid];
   if (tid == 0) {
     *rn_dev = all;
     *rn_eff = min(all, cap);
@@ -426,39 +450,47 @@ __device__ void sort_bucket(const uint64_t* __restrict__ keys, uint32_t* __restr
 
 // NT = 128: buckets up to 2048 entries in n = 128 * E slots (E = 2 .. 16, the smallest
 // that fits), 2049..4096 with E = 32; NT = 1024 (LARGE): 4097..16384 entries.
-template <int NT, bool LARGE>
+template <int NT, int CLS>
 __global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restrict__ ranges,
                                                         const uint64_t* __restrict__ keys,
                                                         uint32_t* __restrict__ tile_vals,
                                                         uint8_t* __restrict__ tile_masks,
                                                         const uint64_t* __restrict__ depth_bits,
                                                         const unsigned long long* __restrict__ depth_minmax,
-                                                        int src_bits) {
+                                                        int src_bits, const int32_t* __restrict__ classes,
+                                                        int tiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* sm = reinterpret_cast<uint64_t*>(smem_raw);
-  const int t = blockIdx.x;
-  const int start = ranges[2 * t], len = ranges[2 * t + 1] - start;
   const int sh = key_shift(depth_minmax, src_bits);
   const uint64_t dmin = depth_minmax[0];
-  if (!LARGE) {
-    if (len < 1 || len > 4096) return;
-    if (len == 1) {  // nothing to sort: unpack the key
-      if (threadIdx.x == 0) {
-        const uint64_t v = keys[start];
-        tile_vals[start] = static_cast<uint32_t>((v & ((1ull << src_bits) - 1ull)) >> kFieldExtra);
-        tile_masks[start] = static_cast<uint8_t>(v);
+  const int n_cls = classes[kSortClasses * tiles + CLS];
+  for (int b = blockIdx.x; b < n_cls; b += gridDim.x) {
+    const int t = classes[CLS * tiles + b];
+    const int start = ranges[2 * t], len = ranges[2 * t + 1] - start;
+    if (CLS == 0) {
+      if (len == 1) {  // nothing to sort: unpack the key
+        if (threadIdx.x == 0) {
+          const uint64_t v = keys[start];
+          tile_vals[start] = static_cast<uint32_t>((v & ((1ull << src_bits) - 1ull)) >> kFieldExtra);
+          tile_masks[start] = static_cast<uint8_t>(v);
+        }
+      } else if (len <= 256) {
+        sort_bucket<NT, 2>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+      } else if (len <= 512) {
+        sort_bucket<NT, 4>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+      } else if (len <= 1024) {
+        sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+      } else if (len <= 2048) {
+        sort_bucket<NT, 16>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+      } else {
+        sort_bucket<NT, 32>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
       }
-      return;
+    } else if (CLS == 1) {
+      sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+    } else {
+      sort_bucket<NT, 16>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
     }
-    if (len <= 256) sort_bucket<NT, 2>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else if (len <= 512) sort_bucket<NT, 4>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else if (len <= 1024) sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else if (len <= 2048) sort_bucket<NT, 16>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else sort_bucket<NT, 32>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
-  } else {
-    if (len <= 4096 || len > 16384) return;
-    if (len <= 8192) sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
-    else sort_bucket<NT, 16>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+    __syncthreads();  // shared memory is reused by the next tile
   }
 }
 
@@ -466,19 +498,11 @@ __global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restric
 // 16384-key chunk in shared memory, then merge-path passes in global memory double the
 // sorted run width until the bucket is one run (ping-pong with `scratch`).
 constexpr int kHugeChunk = 16384;
-__global__ void __launch_bounds__(1024) sort_tiles_huge_kernel(const int32_t* __restrict__ ranges,
-                                                               uint64_t* __restrict__ keys,
-                                                               uint64_t* __restrict__ scratch,
-                                                               uint32_t* __restrict__ tile_vals,
-                                                               uint8_t* __restrict__ tile_masks,
-                                                               const uint64_t* __restrict__ depth_bits,
-                                                               const unsigned long long* __restrict__ depth_minmax,
-                                                               int src_bits) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* sm = reinterpret_cast<uint64_t*>(smem_raw);
-  const int t = blockIdx.x;
+__device__ void sort_huge_bucket(int t, const int32_t* __restrict__ ranges, uint64_t* __restrict__ keys,
+                                 uint64_t* __restrict__ scratch, uint32_t* __restrict__ tile_vals,
+                                 uint8_t* __restrict__ tile_masks, const uint64_t* __restrict__ depth_bits,
+                                 const unsigned long long* __restrict__ depth_minmax, int src_bits, uint64_t* sm) {
   const int start = ranges[2 * t], len = ranges[2 * t + 1] - start;
-  if (len <= kHugeChunk) return;
   constexpr int NT = 1024, E = kHugeChunk / NT;
   uint64_t* src = keys + start;
   uint64_t* dst = scratch + start;
@@ -541,6 +565,25 @@ __global__ void __launch_bounds__(1024) sort_tiles_huge_kernel(const int32_t* __
   if (tie) repair_truncated_runs(tile_vals + start, tile_masks + start, len, depth_bits, depth_minmax[0], sh);
 }
 
+__global__ void __launch_bounds__(1024) sort_tiles_huge_kernel(const int32_t* __restrict__ ranges,
+                                                               uint64_t* __restrict__ keys,
+                                                               uint64_t* __restrict__ scratch,
+                                                               uint32_t* __restrict__ tile_vals,
+                                                               uint8_t* __restrict__ tile_masks,
+                                                               const uint64_t* __restrict__ depth_bits,
+                                                               const unsigned long long* __restrict__ depth_minmax,
+                                                               int src_bits, const int32_t* __restrict__ classes,
+                                                               int tiles) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* sm = reinterpret_cast<uint64_t*>(smem_raw);
+  const int n_cls = classes[kSortClasses * tiles + 3];
+  for (int b = blockIdx.x; b < n_cls; b += gridDim.x) {
+    sort_huge_bucket(classes[3 * tiles + b], ranges, keys, scratch, tile_vals, tile_masks, depth_bits, depth_minmax,
+                     src_bits, sm);
+    __syncthreads();
+  }
+}
+
 __global__ void compact_kernel(const int32_t* __restrict__ valid, const int32_t* __restrict__ pos,
                                const uint64_t* __restrict__ depth_bits, int64_t n, uint64_t* __restrict__ keys_out,
                                uint32_t* __restrict__ src_out) {
@@ -571,9 +614,10 @@ inline unsigned grid_for(int64_t n, int block) { return static_cast<unsigned>((n
 
 void launch_tile_scan(const uint32_t* tile_counts, int tiles, uint32_t cap, int32_t* ranges, uint32_t* cursor,
                       uint32_t* totals, uint32_t* tile_start, uint32_t* rn_dev, uint32_t* rn_eff,
-                      unsigned long long* nonempty, int32_t* overflow, cudaStream_t st) {
+                      unsigned long long* nonempty, int32_t* overflow, int32_t* classes, cudaStream_t st) {
   tile_sub_scan_kernel<<<grid_for(tiles, 256), 256, 0, st>>>(tile_counts, tiles, cursor, totals);
-  tile_scan_kernel<<<1, 1024, 0, st>>>(totals, tiles, cap, ranges, tile_start, rn_dev, rn_eff, nonempty, overflow);
+  tile_scan_kernel<<<1, 1024, 0, st>>>(totals, tiles, cap, ranges, tile_start, rn_dev, rn_eff, nonempty, overflow,
+                                       classes);
 }
 
 void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const BinRec* bins, const DevRaster& rs,
@@ -585,48 +629,61 @@ void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const Bin
                                                   depth_bits, depth_minmax, src_bits, img_w);
 }
 
-template <int NT, bool LARGE>
+template <int NT, int CLS>
 void launch_sort_class(const int32_t* ranges, int tiles, const uint64_t* keys, uint32_t* tile_vals,
-                       uint8_t* tile_masks, const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits,
-                       cudaStream_t st) {
-  constexpr int smem = static_cast<int>(sizeof(uint64_t)) * (LARGE ? 16384 : 4096);
+                       uint8_t* tile_masks, const uint64_t* depth_bits, const unsigned long long* depth_minmax,
+                       int src_bits, const int32_t* classes, int grid, cudaStream_t st) {
+  constexpr int smem = static_cast<int>(sizeof(uint64_t)) * (CLS == 0 ? 4096 : CLS == 1 ? 8192 : 16384);
   static unsigned long long configured = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured >> dev & 1ull)) {
-    cudaFuncSetAttribute(sort_tiles_kernel<NT, LARGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sort_tiles_kernel<NT, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured |= 1ull << dev;
   }
-  sort_tiles_kernel<NT, LARGE><<<tiles, NT, smem, st>>>(ranges, keys, tile_vals, tile_masks, depth_bits, depth_minmax,
-                                                        src_bits);
+  sort_tiles_kernel<NT, CLS><<<std::min(grid, tiles), NT, smem, st>>>(ranges, keys, tile_vals, tile_masks, depth_bits,
+                                                                     depth_minmax, src_bits, classes, tiles);
 }
 
 void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint64_t* key_scratch, uint32_t* tile_vals,
                        uint8_t* tile_masks, const uint64_t* depth_bits, const unsigned long long* depth_minmax,
-                       int src_bits, cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
+                       int src_bits, const int32_t* classes, cudaStream_t st, cudaStream_t side, cudaStream_t side2,
+                       cudaEvent_t fork, cudaEvent_t join, cudaEvent_t join2) {
   if (tiles <= 0) return;
   src_bits += kFieldExtra;  // the keys' source field carries the warp-block mask below the source
-  // The few large buckets (one 1024-thread CTA per SM) run on a side stream, concurrently
-  // with the many small ones, which fit beside them on every SM.
+  static int sms[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int n_sm = sms[dev];
+  // Persistent launches over K3b's class lists. The large classes run on two side streams,
+  // concurrently with the many small buckets, which fit beside them on every SM: side:
+  // the beyond-16384 buckets then the 16384-key class (1 CTA per SM each); side2: the
+  // 8192-key class (3 CTAs per SM).
   cudaEventRecord(fork, st);
   cudaStreamWaitEvent(side, fork, 0);
-  launch_sort_class<1024, true>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits,
-                                side);
+  cudaStreamWaitEvent(side2, fork, 0);
   {
     constexpr int smem = static_cast<int>(sizeof(uint64_t)) * kHugeChunk;
     static unsigned long long configured = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
     if (!(configured >> dev & 1ull)) {
       cudaFuncSetAttribute(sort_tiles_huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       configured |= 1ull << dev;
     }
-    sort_tiles_huge_kernel<<<tiles, 1024, smem, side>>>(ranges, tile_keys, key_scratch, tile_vals, tile_masks,
-                                                        depth_bits, depth_minmax, src_bits);
+    sort_tiles_huge_kernel<<<std::min(n_sm, tiles), 1024, smem, side>>>(ranges, tile_keys, key_scratch, tile_vals,
+                                                                        tile_masks, depth_bits, depth_minmax, src_bits,
+                                                                        classes, tiles);
   }
-  launch_sort_class<128, false>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, st);
+  launch_sort_class<1024, 2>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
+                             n_sm, side);
+  launch_sort_class<1024, 1>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
+                             3 * n_sm, side2);
+  launch_sort_class<128, 0>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
+                            4 * n_sm, st);
   cudaEventRecord(join, side);
+  cudaEventRecord(join2, side2);
   cudaStreamWaitEvent(st, join, 0);
+  cudaStreamWaitEvent(st, join2, 0);
 }
 
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n, uint64_t* keys_out,

@@ -58,8 +58,8 @@ struct psm_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  cudaStream_t side = nullptr;   // concurrent side work within a frame (large tile buckets)
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t side = nullptr, side2 = nullptr;  // concurrent side work within a frame (large tile buckets)
+  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
   cudaStream_t copy = nullptr;   // device-to-host copies of finished row bands (host targets)
   cudaEvent_t band_ev[8] = {};
   cudaEvent_t copy_done = nullptr;
@@ -73,7 +73,7 @@ struct psm_ctx {
   psm::Buf recs, bins, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, kscratch2, valid, pos, keys_c, src_c, keys_s, src_s;
   psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
   psm::Buf lists_w, pan_ids, pan_classes, pan_sem, qclass, lab_tmp, lab_scratch, lab_dist, lab_arg;
-  psm::Buf lists_t, topk_pos, bw_gin, bw_out, tmasks;
+  psm::Buf lists_t, topk_pos, bw_gin, bw_out, tmasks, tclasses;
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
   psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
@@ -221,6 +221,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   if (n > 0) {
     SurfRec* recs; BinRec* bins; uint64_t* dbits; int32_t* valid;
     uint32_t *tcounts, *cursor, *ttotals, *tstart;
+    int32_t* tclasses;
     PSM_TRY(ensure(ctx, ctx->recs, n, &recs));
     PSM_TRY(ensure(ctx, ctx->bins, n, &bins));
     PSM_TRY(ensure(ctx, ctx->depth_bits, n, &dbits));
@@ -229,6 +230,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->cursor, static_cast<size_t>(tiles) * kSplit, &cursor));
     PSM_TRY(ensure(ctx, ctx->tile_totals, tiles, &ttotals));
     PSM_TRY(ensure(ctx, ctx->tile_start, tiles, &tstart));
+    PSM_TRY(ensure(ctx, ctx->tclasses, static_cast<size_t>(tiles) * 5, &tclasses));  // K3b's sort-class lists
     PSM_CUDA_TRY(cudaMemsetAsync(tcounts, 0, sizeof(uint32_t) * tiles * kSplit, st));
     // K1: projection, records, per-tile bucket sizes
     unsigned long long* dminmax;
@@ -243,7 +245,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     // key capacity: sized from the last frame's RN-Total; the first frame reads it (one host sync)
     if (ctx->key_cap == 0) {
       launch_tile_scan(tcounts, tiles, 0xffffffffu, ranges, cursor, ttotals, tstart, rn_dev, rn_eff_dev, small + 1,
-                       key_ovf, st);
+                       key_ovf, tclasses, st);
       uint32_t rn_host = 0;
       PSM_CUDA_TRY(cudaMemcpyAsync(&rn_host, rn_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
       PSM_CUDA_TRY(cudaStreamSynchronize(st));
@@ -263,7 +265,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
 
     // K3: bucket offsets = per-tile ranges, RN-Total, non-empty tiles
     launch_tile_scan(tcounts, tiles, static_cast<uint32_t>(key_cap), ranges, cursor, ttotals, tstart, rn_dev,
-                     rn_eff_dev, small + 1, key_ovf, st);
+                     rn_eff_dev, small + 1, key_ovf, tclasses, st);
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 2);
     // K4: every (surfel, tile) pair into its tile's bucket
@@ -272,8 +274,8 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_CUDA_TRY(cudaGetLastError());
     record(ctx, 3);
     // K5: per-tile sort by (depth bits, source)
-    launch_sort_tiles(ranges, tiles, tkeys, tkeys2, tvals, tmasks, dbits, dminmax, src_bits, st, ctx->side, ctx->fork,
-                      ctx->join);
+    launch_sort_tiles(ranges, tiles, tkeys, tkeys2, tvals, tmasks, dbits, dminmax, src_bits, tclasses, st, ctx->side,
+                      ctx->side2, ctx->fork, ctx->join, ctx->join2);
     PSM_CUDA_TRY(cudaGetLastError());
     tvals_s = tvals;
     tmasks_s = tmasks;
@@ -609,8 +611,10 @@ int psm_create(int device, void* stream, psm_ctx** out) {
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->join2, cudaEventDisableTiming) != cudaSuccess) {
     delete ctx;
     return PSM_ECUDA;
   }
@@ -634,7 +638,7 @@ int psm_destroy(psm_ctx* ctx) {
   psm::Buf* bufs[] = {&ctx->recs, &ctx->bins, &ctx->depth_bits, &ctx->dminmax, &ctx->tile_counts, &ctx->cursor, &ctx->tile_totals, &ctx->tile_start, &ctx->kscratch, &ctx->kscratch2, &ctx->valid, &ctx->pos,
                       &ctx->keys_c, &ctx->src_c, &ctx->keys_s, &ctx->src_s,
                       &ctx->tkeys, &ctx->tvals, &ctx->tkeys2, &ctx->tvals2, &ctx->ranges, &ctx->scan_tmp, &ctx->hist, &ctx->khist, &ctx->totals,
-                      &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg, &ctx->tmasks,
+                      &ctx->dev_small, &ctx->lists, &ctx->rank_of, &ctx->dbg_keys, &ctx->topk_dbg, &ctx->tmasks, &ctx->tclasses,
                       &ctx->lists_w, &ctx->pan_ids, &ctx->pan_classes, &ctx->pan_sem, &ctx->qclass, &ctx->lab_tmp,
                       &ctx->lab_scratch, &ctx->lab_dist, &ctx->lab_arg, &ctx->lists_t, &ctx->topk_pos, &ctx->bw_gin,
                       &ctx->bw_out,
@@ -644,7 +648,9 @@ int psm_destroy(psm_ctx* ctx) {
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   if (ctx->fork) cudaEventDestroy(ctx->fork);
   if (ctx->join) cudaEventDestroy(ctx->join);
+  if (ctx->join2) cudaEventDestroy(ctx->join2);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->side2) cudaStreamDestroy(ctx->side2);
   for (auto& e : ctx->band_ev) if (e) cudaEventDestroy(e);
   if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);

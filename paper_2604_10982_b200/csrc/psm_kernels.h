@@ -92,14 +92,15 @@ void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam,
 // binning.cu
 void launch_tile_scan(const uint32_t* tile_counts, int tiles, uint32_t cap, int32_t* ranges, uint32_t* cursor,
                       uint32_t* totals, uint32_t* tile_start, uint32_t* rn_dev, uint32_t* rn_eff,
-                      unsigned long long* nonempty, int32_t* overflow, cudaStream_t st);
+                      unsigned long long* nonempty, int32_t* overflow, int32_t* classes, cudaStream_t st);
 void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const BinRec* bins, const DevRaster& rs,
                  int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint64_t* tile_keys,
                  const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, int img_w,
                  cudaStream_t st);
 void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, uint64_t* key_scratch, uint32_t* tile_vals,
                        uint8_t* tile_masks, const uint64_t* depth_bits, const unsigned long long* depth_minmax,
-                       int src_bits, cudaStream_t st, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
+                       int src_bits, const int32_t* classes, cudaStream_t st, cudaStream_t side, cudaStream_t side2,
+                       cudaEvent_t fork, cudaEvent_t join, cudaEvent_t join2);
 void launch_compact(const int32_t* valid, const int32_t* pos, const uint64_t* depth_bits, int64_t n,
                     uint64_t* keys_out, uint32_t* src_out, cudaStream_t st);
 void launch_rank_of(const uint32_t* src_by_rank, const uint32_t* n_proj_dev, int64_t cap, int32_t* rank_of,
