@@ -314,7 +314,9 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         if constexpr (KMAX > 0 || FULL_LIST) {
           const int pos = spos[buf * kChunk + j];  // list position; source id = vals[pos]
           if constexpr (KMAX > 0) {
-            if (before(wt, pos, thr_w, thr_p, p.vals)) {  // insertion select (raster.cpp:238-249)
+            // insertion select (raster.cpp:238-249); below the threshold weight (the common
+            // case once the list is full) one compare decides
+            if (wt >= thr_w && before(wt, pos, thr_w, thr_p, p.vals)) {
               int i = n_top < klen ? n_top++ : klen - 1;  // the list fills without a threshold
               while (i > 0) {
                 const double w = top_w[(i - 1) * kThreads + tid];
