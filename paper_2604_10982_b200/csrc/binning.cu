@@ -61,6 +61,9 @@ __device__ __forceinline__ int sort_class(int len) {
   return 3;
 }
 
+// 0 for the longest lists (bit length 32) .. 32 for empty ones
+__device__ __forceinline__ int lpt_bucket(int len) { return __clz(len); }
+
 // K3b: one CTA scans the tile totals: ranges, tile starts, RN-Total, non-empty tiles.
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ totals, int tiles, uint32_t cap,
                                                         int32_t* __restrict__ ranges, uint32_t* __restrict__ tile_start,
@@ -71,7 +74,9 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t warp_ne[32];
   __shared__ int cls_n[kSortClasses];
+  __shared__ int lpt_n[33];
   if (threadIdx.x < kSortClasses) cls_n[threadIdx.x] = 0;
+  if (threadIdx.x < 33) lpt_n[threadIdx.x] = 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int per = (tiles + 1023) / 1024;  // consecutive tiles per thread
   const int t0 = tid * per;
@@ -117,7 +122,26 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
       if (c >= 0) classes[c * tiles + atomicAdd(&cls_n[c], 1)] = t;
     }
   }
+  // Heaviest-first tile order for the blend's work items (longest-processing-time
+  // scheduling by power-of-two bucket of the tile's list length): classes[5 tiles + i].
+  for (int j = 0; j < per; ++j) {
+    const int t = t0 + j;
+    if (t < tiles) atomicAdd(&lpt_n[lpt_bucket(ranges[2 * t + 1] - ranges[2 * t])], 1);
+  }
   __syncthreads();
+  if (tid == 0) {
+    int run_b = 0;
+    for (int b = 0; b < 33; ++b) {
+      const int c = lpt_n[b];
+      lpt_n[b] = run_b;
+      run_b += c;
+    }
+  }
+  __syncthreads();
+  for (int j = 0; j < per; ++j) {
+    const int t = t0 + j;
+    if (t < tiles) classes[5 * tiles + atomicAdd(&lpt_n[lpt_bucket(ranges[2 * t + 1] - ranges[2 * t])], 1)] = t;
+  }
   if (tid < kSortClasses) classes[kSortClasses * tiles + tid] = cls_n[tid];
   if (tid == 0) {
     *rn_dev = all;

@@ -652,8 +652,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(Blend
     if ((threadIdx.x & 31) == 0) item = atomicAdd(p.work, 1);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
-    blend_block<KMAX, FULL_LIST, VEC, NV, LPP, EXACT, PANO_T>(p, p.tile_base + item / kWarps, item % kWarps, stage,
-                                                              exp_tab, top_w, top_p);
+    const int tile = p.order ? __ldg(p.order + item / kWarps) : p.tile_base + item / kWarps;
+    blend_block<KMAX, FULL_LIST, VEC, NV, LPP, EXACT, PANO_T>(p, tile, item % kWarps, stage, exp_tab, top_w, top_p);
     __syncwarp();  // the lanes' Top-K columns and staging are rewritten by the next item
   }
 }

@@ -217,6 +217,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   record(ctx, 0);
   uint32_t* tvals_s = nullptr;
   uint8_t* tmasks_s = nullptr;
+  const int32_t* tclasses_s = nullptr;
   int64_t key_cap = 0;
   if (n > 0) {
     SurfRec* recs; BinRec* bins; uint64_t* dbits; int32_t* valid;
@@ -230,7 +231,8 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->cursor, static_cast<size_t>(tiles) * kSplit, &cursor));
     PSM_TRY(ensure(ctx, ctx->tile_totals, tiles, &ttotals));
     PSM_TRY(ensure(ctx, ctx->tile_start, tiles, &tstart));
-    PSM_TRY(ensure(ctx, ctx->tclasses, static_cast<size_t>(tiles) * 5, &tclasses));  // K3b's sort-class lists
+    // K3b's sort-class lists and counts, and the blend's heaviest-first tile order
+    PSM_TRY(ensure(ctx, ctx->tclasses, static_cast<size_t>(tiles) * 6, &tclasses));
     PSM_CUDA_TRY(cudaMemsetAsync(tcounts, 0, sizeof(uint32_t) * tiles * kSplit, st));
     // K1: projection, records, per-tile bucket sizes
     unsigned long long* dminmax;
@@ -279,6 +281,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_CUDA_TRY(cudaGetLastError());
     tvals_s = tvals;
     tmasks_s = tmasks;
+    tclasses_s = tclasses;
     record(ctx, 4);
   }
   // K7: blend
@@ -340,6 +343,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   }
   if (!on_band) {
     bp.work = reinterpret_cast<int32_t*>(small + 8);
+    if (tclasses_s) bp.order = tclasses_s + 5 * static_cast<int64_t>(tiles);
     launch_blend(bp, tiles, topk, st);
     PSM_CUDA_TRY(cudaGetLastError());
   } else {

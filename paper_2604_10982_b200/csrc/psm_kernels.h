@@ -20,6 +20,7 @@ struct BlendParams {
   int32_t tile_base;      // first tile of this launch (row bands)
   int32_t n_tiles;        // tiles of this launch (set by launch_blend)
   int32_t* work;          // zeroed work counter of this launch: (tile, 8x4 block) items taken
+  const int32_t* order;   // optional: tile of the i-th item group (heaviest first), else tile_base + i
   double cam_cx, cam_cy, cam_fx, cam_fy;
   double chi2, alpha_min, t_min, bg0, bg1, bg2;
   int32_t support_cutoff, render_depth_normal, k_sel;
