@@ -48,17 +48,18 @@ __global__ void __launch_bounds__(256) tile_sub_scan_kernel(const uint32_t* __re
   totals[t] = run;
 }
 
-// Per-tile sort size classes (K5): 0: 1..4096 keys (128 threads), 1: ..8192 and
-// 2: ..16384 (1024 threads, 64 / 128 KB of shared memory), 3: beyond (chunked + global
-// merge passes). K3b lists each class's tiles: classes[c * tiles + i], count at
-// classes[kSortClasses * tiles + c].
-constexpr int kSortClasses = 4;
+// Per-tile sort size classes (K5): 0: 1..1024 keys (128 threads), 1: ..4096 (512
+// threads), 2: ..8192 and 3: ..16384 (1024 threads, 64 / 128 KB of shared memory), 4:
+// beyond (chunked + global merge passes). K3b lists each class's tiles:
+// classes[c * tiles + i], count at classes[kSortClasses * tiles + c]; the blend's
+// heaviest-first order follows at classes[(kSortClasses + 1) * tiles + i].
 __device__ __forceinline__ int sort_class(int len) {
   if (len < 1) return -1;
-  if (len <= 4096) return 0;
-  if (len <= 8192) return 1;
-  if (len <= 16384) return 2;
-  return 3;
+  if (len <= 1024) return 0;
+  if (len <= 4096) return 1;
+  if (len <= 8192) return 2;
+  if (len <= 16384) return 3;
+  return 4;
 }
 
 // 0 for the longest lists (bit length 32) .. 32 for empty ones
@@ -140,7 +141,8 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
   __syncthreads();
   for (int j = 0; j < per; ++j) {
     const int t = t0 + j;
-    if (t < tiles) classes[5 * tiles + atomicAdd(&lpt_n[lpt_bucket(ranges[2 * t + 1] - ranges[2 * t])], 1)] = t;
+    if (t < tiles)
+      classes[(kSortClasses + 1) * tiles + atomicAdd(&lpt_n[lpt_bucket(ranges[2 * t + 1] - ranges[2 * t])], 1)] = t;
   }
   if (tid < kSortClasses) classes[kSortClasses * tiles + tid] = cls_n[tid];
   if (tid == 0) {
@@ -502,14 +504,13 @@ __global__ void __launch_bounds__(NT) sort_tiles_kernel(const int32_t* __restric
         sort_bucket<NT, 2>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
       } else if (len <= 512) {
         sort_bucket<NT, 4>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
-      } else if (len <= 1024) {
-        sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
-      } else if (len <= 2048) {
-        sort_bucket<NT, 16>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
       } else {
-        sort_bucket<NT, 32>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+        sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
       }
-    } else if (CLS == 1) {
+    } else if (CLS == 1) {  // NT = 512
+      if (len <= 2048) sort_bucket<NT, 4>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+      else sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
+    } else if (CLS == 2) {
       sort_bucket<NT, 8>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
     } else {
       sort_bucket<NT, 16>(keys, tile_vals, tile_masks, start, len, sm, depth_bits, dmin, sh, src_bits);
@@ -600,9 +601,9 @@ __global__ void __launch_bounds__(1024) sort_tiles_huge_kernel(const int32_t* __
                                                                int tiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* sm = reinterpret_cast<uint64_t*>(smem_raw);
-  const int n_cls = classes[kSortClasses * tiles + 3];
+  const int n_cls = classes[kSortClasses * tiles + 4];
   for (int b = blockIdx.x; b < n_cls; b += gridDim.x) {
-    sort_huge_bucket(classes[3 * tiles + b], ranges, keys, scratch, tile_vals, tile_masks, depth_bits, depth_minmax,
+    sort_huge_bucket(classes[4 * tiles + b], ranges, keys, scratch, tile_vals, tile_masks, depth_bits, depth_minmax,
                      src_bits, sm);
     __syncthreads();
   }
@@ -657,7 +658,7 @@ template <int NT, int CLS>
 void launch_sort_class(const int32_t* ranges, int tiles, const uint64_t* keys, uint32_t* tile_vals,
                        uint8_t* tile_masks, const uint64_t* depth_bits, const unsigned long long* depth_minmax,
                        int src_bits, const int32_t* classes, int grid, cudaStream_t st) {
-  constexpr int smem = static_cast<int>(sizeof(uint64_t)) * (CLS == 0 ? 4096 : CLS == 1 ? 8192 : 16384);
+  constexpr int smem = static_cast<int>(sizeof(uint64_t)) * (CLS <= 1 ? NT * 8 : CLS == 2 ? 8192 : 16384);
   static unsigned long long configured = 0;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -698,12 +699,14 @@ void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, ui
                                                                         tile_masks, depth_bits, depth_minmax, src_bits,
                                                                         classes, tiles);
   }
-  launch_sort_class<1024, 2>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
+  launch_sort_class<1024, 3>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
                              n_sm, side);
-  launch_sort_class<1024, 1>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
+  launch_sort_class<1024, 2>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
                              3 * n_sm, side2);
+  launch_sort_class<512, 1>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
+                            4 * n_sm, side2);
   launch_sort_class<128, 0>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
-                            4 * n_sm, st);
+                            8 * n_sm, st);
   cudaEventRecord(join, side);
   cudaEventRecord(join2, side2);
   cudaStreamWaitEvent(st, join, 0);

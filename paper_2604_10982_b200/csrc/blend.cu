@@ -37,8 +37,7 @@ namespace psm {
 namespace {
 
 constexpr int kTile = 16;
-constexpr int kThreads = kTile * kTile;
-constexpr int kWarps = kThreads / 32;
+constexpr int kBlocks = 8;  // 8x4 pixel blocks (work items) per 16x16 tile
 constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
 
 // Kernel shape per Top-K width: records per warp chunk (double-buffered) and resident
@@ -64,6 +63,20 @@ constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
 #ifndef PSM_BLEND_MB32
 #define PSM_BLEND_MB32 2
 #endif
+#ifndef PSM_BLEND_W8
+#define PSM_BLEND_W8 8
+#endif
+#ifndef PSM_BLEND_W16
+#define PSM_BLEND_W16 8
+#endif
+#ifndef PSM_BLEND_W32
+#define PSM_BLEND_W32 8
+#endif
+// warps per CTA (each pulls its own work items; the count only sets residency and registers)
+__host__ __device__ constexpr int cta_warps(int kmax) {
+  return kmax == 0 ? 8 : (kmax <= 8 ? PSM_BLEND_W8 : (kmax <= 16 ? PSM_BLEND_W16 : PSM_BLEND_W32));
+}
+__host__ __device__ constexpr int cta_threads(int kmax) { return 32 * cta_warps(kmax); }
 __host__ __device__ constexpr int chunk_for(int kmax) {
   return kmax == 0 ? 30 : (kmax <= 8 ? PSM_BLEND_CH8 : (kmax <= 16 ? PSM_BLEND_CH16 : PSM_BLEND_CH32));
 }
@@ -82,9 +95,11 @@ constexpr size_t kExpTabBytes = 256 * sizeof(uint64_t);
 __host__ __device__ constexpr size_t warp_stage_bytes(int kmax) {
   return (2 * chunk_for(kmax) * (sizeof(SurfRec) + sizeof(int)) + 15) / 16 * 16;
 }
-__host__ __device__ constexpr size_t stage_bytes(int kmax) { return static_cast<size_t>(kWarps) * warp_stage_bytes(kmax); }
+__host__ __device__ constexpr size_t stage_bytes(int kmax) {
+  return static_cast<size_t>(cta_warps(kmax)) * warp_stage_bytes(kmax);
+}
 __host__ __device__ constexpr size_t smem_bytes(int kmax) {
-  return stage_bytes(kmax) + kExpTabBytes + static_cast<size_t>(kmax) * kThreads * (sizeof(double) + sizeof(int));
+  return stage_bytes(kmax) + kExpTabBytes + static_cast<size_t>(kmax) * cta_threads(kmax) * (sizeof(double) + sizeof(int));
 }
 static_assert(smem_bytes(8) * PSM_BLEND_MB8 + 1024 * PSM_BLEND_MB8 <= 228 * 1024, "K=8 shape exceeds shared memory");
 static_assert(smem_bytes(16) * PSM_BLEND_MB16 + 1024 * PSM_BLEND_MB16 <= 228 * 1024, "K=16 shape exceeds shared memory");
@@ -144,6 +159,7 @@ template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT, int PA
 __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile, const int blk, SurfRec* stage,
                                             const uint64_t* exp_tab, double* top_w, int* top_p) {
   constexpr int kChunk = chunk_for(KMAX);
+  constexpr int kCT = cta_threads(KMAX);  // Top-K column stride
   const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -319,18 +335,18 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
             if (wt >= thr_w && before(wt, pos, thr_w, thr_p, p.vals)) {
               int i = n_top < klen ? n_top++ : klen - 1;  // the list fills without a threshold
               while (i > 0) {
-                const double w = top_w[(i - 1) * kThreads + tid];
-                const int q = top_p[(i - 1) * kThreads + tid];
+                const double w = top_w[(i - 1) * kCT + tid];
+                const int q = top_p[(i - 1) * kCT + tid];
                 if (!before(wt, pos, w, q, p.vals)) break;
-                top_w[i * kThreads + tid] = w;
-                top_p[i * kThreads + tid] = q;
+                top_w[i * kCT + tid] = w;
+                top_p[i * kCT + tid] = q;
                 --i;
               }
-              top_w[i * kThreads + tid] = wt;
-              top_p[i * kThreads + tid] = pos;
+              top_w[i * kCT + tid] = wt;
+              top_p[i * kCT + tid] = pos;
               if (n_top == klen) {
-                thr_w = top_w[(klen - 1) * kThreads + tid];
-                thr_p = top_p[(klen - 1) * kThreads + tid];
+                thr_w = top_w[(klen - 1) * kCT + tid];
+                thr_p = top_p[(klen - 1) * kCT + tid];
               }
             }
           }
@@ -390,14 +406,14 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       if (p.topk_dbg) {
         for (int i = 0; i < k_sel; ++i)
           p.topk_dbg[pix * k_sel + i] =
-              i < blend_n ? static_cast<int>(__ldg(p.vals + top_p[i * kThreads + tid])) : -1;
+              i < blend_n ? static_cast<int>(__ldg(p.vals + top_p[i * kCT + tid])) : -1;
       }
     }
     if constexpr (FULL_LIST) {
       if (m > p.list_cap) atomicMax(p.list_overflow, m);
       if constexpr (KMAX > 0) {  // backward cache: the selected list positions
         if (p.topk_pos)
-          for (int i = 0; i < blend_n; ++i) p.topk_pos[pix * k_sel + i] = top_p[i * kThreads + tid];
+          for (int i = 0; i < blend_n; ++i) p.topk_pos[pix * k_sel + i] = top_p[i * kCT + tid];
       }
     }
     // ins_argmax stays -1 unless labels were accumulated (raster.cpp:292,497)
@@ -439,8 +455,8 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       if constexpr (KMAX > 0) {
         const int qt = (tid & ~31) + q;  // the pixel's thread: its Top-K list column
         for (int i = 0; i < nq; ++i) {
-          const int s = static_cast<int>(__ldg(p.vals + top_p[i * kThreads + qt]));
-          const float w = static_cast<float>(top_w[i * kThreads + qt]);
+          const int s = static_cast<int>(__ldg(p.vals + top_p[i * kCT + qt]));
+          const float w = static_cast<float>(top_w[i * kCT + qt]);
           const TV* row = reinterpret_cast<const TV*>(p.feat + static_cast<int64_t>(s) * D);
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
@@ -524,16 +540,16 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
   if constexpr (PANO_T > 0) {
     if constexpr (KMAX > 0) {  // selected entries back into blend (list position) order
       for (int i = 1; i < blend_n; ++i) {
-        const int pi = top_p[i * kThreads + tid];
-        const double wi = top_w[i * kThreads + tid];
+        const int pi = top_p[i * kCT + tid];
+        const double wi = top_w[i * kCT + tid];
         int j = i - 1;
-        while (j >= 0 && top_p[j * kThreads + tid] > pi) {
-          top_p[(j + 1) * kThreads + tid] = top_p[j * kThreads + tid];
-          top_w[(j + 1) * kThreads + tid] = top_w[j * kThreads + tid];
+        while (j >= 0 && top_p[j * kCT + tid] > pi) {
+          top_p[(j + 1) * kCT + tid] = top_p[j * kCT + tid];
+          top_w[(j + 1) * kCT + tid] = top_w[j * kCT + tid];
           --j;
         }
-        top_p[(j + 1) * kThreads + tid] = pi;
-        top_w[(j + 1) * kThreads + tid] = wi;
+        top_p[(j + 1) * kCT + tid] = pi;
+        top_w[(j + 1) * kCT + tid] = wi;
       }
     }
     __syncwarp();
@@ -564,8 +580,8 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         int src = 0;
         double sw = 0.0;
         if (lane < nq && D > 0) {
-          src = static_cast<int>(__ldg(p.vals + top_p[i_l * kThreads + (tid & ~31) + q]));
-          sw = top_w[i_l * kThreads + (tid & ~31) + q];
+          src = static_cast<int>(__ldg(p.vals + top_p[i_l * kCT + (tid & ~31) + q]));
+          sw = top_w[i_l * kCT + (tid & ~31) + q];
         }
 #pragma unroll
         for (int i = 0; i < KMAX; ++i) {
@@ -635,25 +651,26 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
 // a frame). A warp's shared memory (staging, Top-K columns) is private to it; the exp
 // table is loaded once per CTA.
 template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT, int PANO_T>
-__global__ void __launch_bounds__(kThreads, min_blocks(KMAX)) blend_kernel(BlendParams p) {
+__global__ void __launch_bounds__(cta_threads(KMAX), min_blocks(KMAX)) blend_kernel(BlendParams p) {
   constexpr int kChunk = chunk_for(KMAX);
+  constexpr int kCT = cta_threads(KMAX);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SurfRec* stage = reinterpret_cast<SurfRec*>(smem_raw + (threadIdx.x >> 5) * warp_stage_bytes(KMAX));  // [2][kChunk]
   // psm_exp's 2^(i/128) table, one copy per CTA (random per-lane lookups: shared memory, not L1)
   uint64_t* exp_tab = reinterpret_cast<uint64_t*>(smem_raw + stage_bytes(KMAX));
   // per-pixel Top-K lists (slot-major: [slot][thread], conflict-free): weights and list positions
   double* top_w = reinterpret_cast<double*>(exp_tab + 256);
-  int* top_p = reinterpret_cast<int*>(top_w + KMAX * kThreads);
-  exp_tab[threadIdx.x] = psm_exp_tab_dev[threadIdx.x];
+  int* top_p = reinterpret_cast<int*>(top_w + KMAX * kCT);
+  for (int i = threadIdx.x; i < 256; i += kCT) exp_tab[i] = psm_exp_tab_dev[i];
   __syncthreads();
-  const int n_items = p.n_tiles * kWarps;
+  const int n_items = p.n_tiles * kBlocks;
   for (;;) {
     int item = 0;
     if ((threadIdx.x & 31) == 0) item = atomicAdd(p.work, 1);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
-    const int tile = p.order ? __ldg(p.order + item / kWarps) : p.tile_base + item / kWarps;
-    blend_block<KMAX, FULL_LIST, VEC, NV, LPP, EXACT, PANO_T>(p, tile, item % kWarps, stage, exp_tab, top_w, top_p);
+    const int tile = p.order ? __ldg(p.order + item / kBlocks) : p.tile_base + item / kBlocks;
+    blend_block<KMAX, FULL_LIST, VEC, NV, LPP, EXACT, PANO_T>(p, tile, item % kBlocks, stage, exp_tab, top_w, top_p);
     __syncwarp();  // the lanes' Top-K columns and staging are rewritten by the next item
   }
 }
@@ -673,7 +690,7 @@ void launch_t(const BlendParams& p, int tiles, cudaStream_t st) {
   const int grid = std::min(tiles, sms[dev] * min_blocks(KMAX));
   BlendParams q = p;
   q.n_tiles = tiles;
-  kern<<<grid, kThreads, smem_bytes(KMAX), st>>>(q);
+  kern<<<grid, cta_threads(KMAX), smem_bytes(KMAX), st>>>(q);
 }
 
 // Feature-lane shapes: float4 lanes, 32/LPP pixels per warp iteration for the

@@ -232,7 +232,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->tile_totals, tiles, &ttotals));
     PSM_TRY(ensure(ctx, ctx->tile_start, tiles, &tstart));
     // K3b's sort-class lists and counts, and the blend's heaviest-first tile order
-    PSM_TRY(ensure(ctx, ctx->tclasses, static_cast<size_t>(tiles) * 6, &tclasses));
+    PSM_TRY(ensure(ctx, ctx->tclasses, static_cast<size_t>(tiles) * (psm::kSortClasses + 2), &tclasses));
     PSM_CUDA_TRY(cudaMemsetAsync(tcounts, 0, sizeof(uint32_t) * tiles * kSplit, st));
     // K1: projection, records, per-tile bucket sizes
     unsigned long long* dminmax;
@@ -343,7 +343,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   }
   if (!on_band) {
     bp.work = reinterpret_cast<int32_t*>(small + 8);
-    if (tclasses_s) bp.order = tclasses_s + 5 * static_cast<int64_t>(tiles);
+    if (tclasses_s) bp.order = tclasses_s + (psm::kSortClasses + 1) * static_cast<int64_t>(tiles);
     launch_blend(bp, tiles, topk, st);
     PSM_CUDA_TRY(cudaGetLastError());
   } else {

@@ -41,6 +41,9 @@ constexpr int kSplit = 32;
 // Bits below the source id in a tile sort key: the 8-bit warp-block live mask of the
 // (surfel, tile) entry (psm_block_mask), carried through the sort beside the source.
 constexpr int kFieldExtra = 8;
+// K5 per-tile sort size classes (binning.cu); K3b writes their tile lists and the
+// blend's tile order into one buffer of (kSortClasses + 2) x tiles ints.
+constexpr int kSortClasses = 5;
 
 // Camera by value in kernel parameters.
 struct DevCamera {
