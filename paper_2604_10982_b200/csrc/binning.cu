@@ -230,7 +230,19 @@ __device__ __forceinline__ uint32_t block_mask_f(const float* sxl, const float* 
   return m;
 }
 
-__global__ void __launch_bounds__(256, 3) emit_kernel(const int32_t* __restrict__ valid, int64_t n,
+// K4, load-balanced: a warp takes 32 surfels, stages each one's key and ellipse
+// constants in shared memory, and then spreads the warp's (surfel, tile row) pairs over
+// its lanes (a surfel covers 1..100+ tiles, so one thread per surfel leaves most lanes
+// idle behind the largest footprint). Tile indices are < 2^19 (checked on the host).
+struct EmitItem {
+  uint64_t key;
+  PsmEllipse e;
+  StripF sf;
+  int tx0, tx1, ty0, strips;
+};
+constexpr int kEmitWarps = 8;
+
+__global__ void __launch_bounds__(32 * kEmitWarps) emit_kernel(const int32_t* __restrict__ valid, int64_t n,
                                                    const SurfRec* __restrict__ recs, const BinRec* __restrict__ bins,
                                                    DevRaster rs, int img_h, uint32_t* __restrict__ cursor,
                                                    const uint32_t* __restrict__ tile_start, uint32_t cap,
@@ -238,47 +250,82 @@ __global__ void __launch_bounds__(256, 3) emit_kernel(const int32_t* __restrict_
                                                    const uint64_t* __restrict__ depth_bits,
                                                    const unsigned long long* __restrict__ depth_minmax, int src_bits,
                                                    int img_w) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n || !valid[i]) return;
-  // the key's source field is (source << 8 | block mask), kFieldExtra bits wider than the source
-  const int fb = src_bits + kFieldExtra;
-  const uint64_t key = sort_key(depth_bits[i], static_cast<uint32_t>(i) << kFieldExtra, depth_minmax[0],
-                                key_shift(depth_minmax, fb), fb);
-  const BinRec b = bins[i];
-  if (b.tx0 > b.tx1 || b.ty0 > b.ty1) return;
+  __shared__ EmitItem items[kEmitWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * kEmitWarps + warp) * 32 + lane;
   const bool ellipse = rs.binning == PSM_BIN_ELLIPSE;
   // warp-block masks need the support cutoff (a pixel only uses candidates passing it)
   const bool masks_on = rs.support_cutoff != 0;
-  PsmEllipse e;
-  if (ellipse || masks_on) e = psm_ellipse_prep(recs[i].cx, recs[i].cy, b.F00, b.F01, b.F11, rs.chi2);
-  StripF sf;
-  const bool strips = masks_on && strip_prep(e, &sf);
-  float sxl[4], sxr[4];
-  uint32_t* cur = cursor + static_cast<int64_t>(threadIdx.x & (kSplit - 1)) * rs.tiles_x * rs.tiles_y;
+  int rows = 0;
+  if (i < n && valid[i]) {
+    const BinRec b = bins[i];
+    if (b.tx0 <= b.tx1 && b.ty0 <= b.ty1) {
+      EmitItem& it = items[warp][lane];
+      // the key's source field is (source << 8 | block mask), kFieldExtra bits wider than the source
+      const int fb = src_bits + kFieldExtra;
+      it.key = sort_key(depth_bits[i], static_cast<uint32_t>(i) << kFieldExtra, depth_minmax[0],
+                        key_shift(depth_minmax, fb), fb);
+      if (ellipse || masks_on) {
+        it.e = psm_ellipse_prep(recs[i].cx, recs[i].cy, b.F00, b.F01, b.F11, rs.chi2);
+      } else {
+        it.e.ok = 0;
+      }
+      it.strips = masks_on && strip_prep(it.e, &it.sf);
+      it.tx0 = b.tx0;
+      it.tx1 = b.tx1;
+      it.ty0 = b.ty0;
+      rows = b.ty1 - b.ty0 + 1;
+    }
+  }
+  // exclusive prefix of the row counts over the warp
+  int incl = rows;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int start = incl - rows;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  __syncwarp();
+
+  // a pair's sub-bucket is its surfel's lane (K1 counted it there: source & (kSplit - 1))
+  const int64_t n_tiles = static_cast<int64_t>(rs.tiles_x) * rs.tiles_y;
   // tiles are claimed in batches of kBatch so several returning atomics are in flight at once
   constexpr int kBatch = 8;
-  uint32_t pend[kBatch];  // tile index | block mask << 24
+  uint32_t pend[kBatch];  // tile index | owner lane << 19 | block mask << 24
   int np = 0;
   auto flush = [&]() {
     uint32_t o[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; ++u)
-      if (u < np) o[u] = atomicAdd(cur + (pend[u] & 0xffffffu), 1u);
+      if (u < np) o[u] = atomicAdd(cursor + ((pend[u] >> 19) & 31u) * n_tiles + (pend[u] & 0x7ffffu), 1u);
 #pragma unroll
     for (int u = 0; u < kBatch; ++u)
       if (u < np) {
-        const uint32_t at = __ldg(tile_start + (pend[u] & 0xffffffu)) + o[u];
-        if (at < cap) tile_keys[at] = key | (pend[u] >> 24);
+        const uint32_t at = __ldg(tile_start + (pend[u] & 0x7ffffu)) + o[u];
+        if (at < cap) tile_keys[at] = items[warp][(pend[u] >> 19) & 31u].key | (pend[u] >> 24);
       }
     np = 0;
   };
-  for (int ty = b.ty0; ty <= b.ty1; ++ty) {
-    int lo = b.tx0, hi = b.tx1;
-    if (ellipse && !psm_ellipse_row(e, ty, rs.tile_size, img_h, b.tx0, b.tx1, &lo, &hi)) continue;
-    if (strips) strips_f(sf, ty, img_h, sxl, sxr);
+  for (int q0 = 0; q0 < total; q0 += 32) {
+    const int q = q0 + lane;
+    int l = 0;  // owner: the last lane whose first pair is <= q
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int s = __shfl_sync(0xffffffffu, start, l + step);
+      if (s <= q) l += step;
+    }
+    const int ls = __shfl_sync(0xffffffffu, start, l);
+    if (q >= total) continue;
+    const EmitItem& it = items[warp][l];
+    const int ty = it.ty0 + (q - ls);
+    int lo = it.tx0, hi = it.tx1;
+    if (ellipse && !psm_ellipse_row(it.e, ty, rs.tile_size, img_h, it.tx0, it.tx1, &lo, &hi)) continue;
+    float sxl[4], sxr[4];
+    if (it.strips) strips_f(it.sf, ty, img_h, sxl, sxr);
     for (int tx = lo; tx <= hi; ++tx) {
-      const uint32_t bm = strips ? block_mask_f(sxl, sxr, tx, img_w) : 0xffu;
-      pend[np++] = static_cast<uint32_t>(ty * rs.tiles_x + tx) | bm << 24;
+      const uint32_t bm = it.strips ? block_mask_f(sxl, sxr, tx, img_w) : 0xffu;
+      pend[np++] = static_cast<uint32_t>(ty * rs.tiles_x + tx) | static_cast<uint32_t>(l) << 19 | bm << 24;
       if (np == kBatch) flush();
     }
   }
@@ -650,8 +697,9 @@ void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const Bin
                  const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, int img_w,
                  cudaStream_t st) {
   if (n > 0)
-    emit_kernel<<<grid_for(n, 256), 256, 0, st>>>(valid, n, recs, bins, rs, img_h, cursor, tile_start, cap, tile_keys,
-                                                  depth_bits, depth_minmax, src_bits, img_w);
+    emit_kernel<<<grid_for(n, 32 * kEmitWarps), 32 * kEmitWarps, 0, st>>>(valid, n, recs, bins, rs, img_h, cursor,
+                                                                          tile_start, cap, tile_keys, depth_bits,
+                                                                          depth_minmax, src_bits, img_w);
 }
 
 template <int NT, int CLS>

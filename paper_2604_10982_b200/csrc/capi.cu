@@ -181,6 +181,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   const int ts = cfg->tile_size;
   const int tiles_x = (W + ts - 1) / ts, tiles_y = (H + ts - 1) / ts;
   const int tiles = tiles_x * tiles_y;
+  if (tiles >= (1 << 19)) return fail(ctx, PSM_EUNSUPPORTED, "image has 2^19 or more 16x16 tiles");
   const int feat_dims = sc->c_sem + sc->n_q;
   const bool topk = cfg->blending == PSM_BLEND_TOPK;
   const int k_sel = cfg->top_k > 1 ? cfg->top_k : 1;
