@@ -193,6 +193,47 @@ def test_gpu_random_surfels(rend):
         assert_parity(rend, sc, None, cam, cfg)
 
 
+def test_gpu_extreme_footprints(rend):
+    """Needles, grazing views, sub-pixel and near-plane (huge) surfels, centres far off-screen
+    with footprints reaching in, on a ragged image: stresses the fp32 warp-block masks (their
+    margins must never drop a candidate whose fp64 support test passes) and the tile rows."""
+    rng = Rng(23)
+    rows = []
+    for i in range(900):
+        kind = i % 6
+        if kind == 0:    # needles at random orientation
+            c = (rng.uniform(-1, 1), rng.uniform(-0.8, 0.8), rng.uniform(1, 5))
+            s1, s2 = rng.uniform(0.3, 2.0), rng.uniform(0.0005, 0.003)
+        elif kind == 1:  # nearly edge-on to the camera
+            c = (rng.uniform(-1, 1), rng.uniform(-0.8, 0.8), rng.uniform(1, 5))
+            s1, s2 = rng.uniform(0.05, 0.5), rng.uniform(0.05, 0.5)
+        elif kind == 2:  # sub-pixel
+            c = (rng.uniform(-1, 1), rng.uniform(-0.8, 0.8), rng.uniform(2, 8))
+            s1, s2 = rng.uniform(0.0005, 0.004), rng.uniform(0.0005, 0.004)
+        elif kind == 3:  # close to the near plane: footprints far larger than the image
+            c = (rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3), rng.uniform(0.12, 0.4))
+            s1, s2 = rng.uniform(0.05, 0.3), rng.uniform(0.01, 0.3)
+        elif kind == 4:  # centre well off-screen, large enough to reach in
+            c = (rng.uniform(2.0, 4.0) * (1 if rng.uniform() < 0.5 else -1), rng.uniform(-1, 1), rng.uniform(1.5, 3))
+            s1, s2 = rng.uniform(1.0, 3.0), rng.uniform(0.05, 1.0)
+        else:            # ordinary
+            c = (rng.uniform(-1, 1), rng.uniform(-0.8, 0.8), rng.uniform(1, 6))
+            s1, s2 = rng.uniform(0.02, 0.3), rng.uniform(0.02, 0.3)
+        q = rng.unit_quaternion()
+        if kind == 1:  # rotate about y by ~90 degrees: the surfel plane almost contains the view ray
+            a = math.pi / 2 * rng.uniform(0.97, 0.999) / 2
+            q = (math.cos(a), 0.0, math.sin(a), 0.0)
+        rows.append(facing_surfel(c, s1, s2, rng.uniform(0.2, 1.0), (rng.uniform(), rng.uniform(), rng.uniform()),
+                                  quat=q))
+    sc = SceneMap(np.array(rows), np.array([[rng.normal() for _ in range(32)] for _ in rows]))
+    cam = front_camera(100, 70, 90.0)
+    for cfg in (RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=8),
+                RasterConfig(binning=Binning.Aabb, blending=Blending.Full),
+                RasterConfig(binning=Binning.Circle, blending=Blending.TopK, top_k=16, chi2=16.0)):
+        g, _ = assert_parity(rend, sc, None, cam, cfg)
+        assert g.blended_total > 0
+
+
 def test_gpu_permutation_bit_identical(rend):
     sc, labels, cam = make_street_scene(StreetSpec(n_surfels=2000, image_w=96, image_h=64, c_sem=3,
                                                    n_instances=8))
