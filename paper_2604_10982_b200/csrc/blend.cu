@@ -177,7 +177,8 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
   int m = 0;
   bool done = !inside;
   float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
-  double exp_depth = 0, dom_depth = 0, dom_w = 0;
+  double exp_depth = 0, dom_w = 0;
+  float dom_depth = 0.f;  // rcp of the strictly-first maximum weight (the plane is fp32)
   // Top-K: the k_sel best (weight desc, source asc) so far live in shared memory; the
   // registers only hold the admission threshold (the k_sel-th entry).
   const int klen = p.k_sel < 1 ? 1 : p.k_sel;
@@ -194,7 +195,8 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
   const unsigned lt_mask = (1u << lane) - 1u;
   int wb = start;
   uint32_t cv = 0, nv = 0;
-  unsigned cm = 0, nm = 0;
+  unsigned nm = 0;  // the next window's mask byte
+  unsigned cm = 0;
   if (start + lane < end) {
     cv = __ldg(p.vals + start + lane);
     cm = __ldg(p.masks + start + lane);
@@ -213,8 +215,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         if (wb + 32 >= end) break;
         wb += 32;
         cv = nv;
-        cm = nm;
-        clive = __ballot_sync(0xffffffffu, wb + lane < end && (!p.support_cutoff || (cm & bbit)));
+        clive = __ballot_sync(0xffffffffu, wb + lane < end && (!p.support_cutoff || (nm & bbit)));
         const int nxt = wb + 32 + lane;
         if (nxt < end) {
           nv = __ldg(p.vals + nxt);
@@ -325,7 +326,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         exp_depth += wt * rcp;
         if (wt > dom_w) {
           dom_w = wt;
-          dom_depth = rcp;
+          dom_depth = static_cast<float>(rcp);
         }
         if constexpr (KMAX > 0 || FULL_LIST) {
           const int pos = spos[buf * kChunk + j];  // list position; source id = vals[pos]
@@ -396,7 +397,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     p.color[pix * 3 + 2] = acc_b + static_cast<float>(T * p.bg2);
     const bool rdn = p.render_depth_normal != 0;
     p.depth[pix * 2 + 0] = rdn ? static_cast<float>(exp_depth) : 0.f;
-    p.depth[pix * 2 + 1] = rdn ? static_cast<float>(dom_depth) : 0.f;
+    p.depth[pix * 2 + 1] = rdn ? dom_depth : 0.f;
     p.normal[pix * 3 + 0] = rdn ? nx : 0.f;
     p.normal[pix * 3 + 1] = rdn ? ny : 0.f;
     p.normal[pix * 3 + 2] = rdn ? nz : 0.f;
