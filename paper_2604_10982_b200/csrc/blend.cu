@@ -194,17 +194,14 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
   const unsigned bbit = 1u << blk;
   const unsigned lt_mask = (1u << lane) - 1u;
   int wb = start;
-  uint32_t cv = 0, nv = 0;
+  uint32_t cv = 0;
   unsigned nm = 0;  // the next window's mask byte
   unsigned cm = 0;
   if (start + lane < end) {
     cv = __ldg(p.vals + start + lane);
     cm = __ldg(p.masks + start + lane);
   }
-  if (start + 32 + lane < end) {
-    nv = __ldg(p.vals + start + 32 + lane);
-    nm = __ldg(p.masks + start + 32 + lane);
-  }
+  if (start + 32 + lane < end) nm = __ldg(p.masks + start + 32 + lane);
   unsigned clive = __ballot_sync(0xffffffffu, start + lane < end && (cm & bbit));
   if (!p.support_cutoff) clive = __ballot_sync(0xffffffffu, start + lane < end);
   // Stages the next (up to) kChunk live entries into buffer `bf`; returns how many.
@@ -214,13 +211,10 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       if (!clive) {
         if (wb + 32 >= end) break;
         wb += 32;
-        cv = nv;
         clive = __ballot_sync(0xffffffffu, wb + lane < end && (!p.support_cutoff || (nm & bbit)));
+        cv = (clive >> lane & 1u) ? __ldg(p.vals + wb + lane) : 0u;
         const int nxt = wb + 32 + lane;
-        if (nxt < end) {
-          nv = __ldg(p.vals + nxt);
-          nm = __ldg(p.masks + nxt);
-        }
+        if (nxt < end) nm = __ldg(p.masks + nxt);
         continue;
       }
       const int r = __popc(clive & lt_mask);
