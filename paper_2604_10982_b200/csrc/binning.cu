@@ -732,7 +732,7 @@ void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, ui
   // Persistent launches over K3b's class lists. The large classes run on two side streams,
   // concurrently with the many small buckets, which fit beside them on every SM: side:
   // the beyond-16384 buckets then the 16384-key class (1 CTA per SM each); side2: the
-  // 8192-key class (3 CTAs per SM).
+  // 8192-key class (3 CTAs per SM); main: the <= 1024 then the <= 4096-key classes.
   cudaEventRecord(fork, st);
   cudaStreamWaitEvent(side, fork, 0);
   cudaStreamWaitEvent(side2, fork, 0);
@@ -752,7 +752,7 @@ void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, ui
   launch_sort_class<1024, 2>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
                              3 * n_sm, side2);
   launch_sort_class<512, 1>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
-                            4 * n_sm, side2);
+                            4 * n_sm, st);
   launch_sort_class<128, 0>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
                             8 * n_sm, st);
   cudaEventRecord(join, side);
