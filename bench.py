@@ -378,10 +378,10 @@ def run_ours(args):
                      "peak_source": peak_src, "alg_bytes_per_launch": b_blend, "launch_ms": blend_avg},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": (9 if pano else 8) * args.steps,
-        "gpu_launches_note": "per step: preprocess, tile_sub_scan, tile_scan, emit, sort_tiles<1024>, "
-                             "sort_tiles_huge, sort_tiles<128>, blend (+3 memsets, 1 small H2D)"
-                             + ("; c3p adds assign_labels" if pano else ""),
+        "gpu_launches": (11 if pano else 10) * args.steps * len(cams),
+        "gpu_launches_note": "per frame: preprocess, tile_sub_scan, tile_scan, emit, sort_tiles_huge, "
+                             "sort_tiles<1024,3>, sort_tiles<1024,2>, sort_tiles<512,1>, sort_tiles<128,0>, blend "
+                             "(+3 memsets, 1 small H2D, 1 small D2H)" + ("; c3p adds assign_labels" if pano else ""),
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
