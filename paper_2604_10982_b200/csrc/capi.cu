@@ -171,7 +171,10 @@ int check_config(psm_ctx* ctx, const psm_raster_config* cfg, int feat_dims) {
 // on_band(band, y0, y1) is called after each band's launch (it queues that band's
 // device-to-host copies on the copy stream, overlapping the next band's blend).
 using BandHook = std::function<int(int band, int y0, int y1)>;
-constexpr int kHostBands = 4;
+#ifndef PSM_HOST_BANDS
+#define PSM_HOST_BANDS 8
+#endif
+constexpr int kHostBands = PSM_HOST_BANDS;  // <= 8 (band events, work counters small[8..16))
 
 int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
                 const Planes& pl, psm_debug* dbg, const BandHook* on_band = nullptr) {
