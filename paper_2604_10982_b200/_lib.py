@@ -9,7 +9,8 @@ import os
 
 from . import _abi as A
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpsm.so")
+# PSM_LIB_PATH selects another build of the same library (A/B kernel variants under scratch/)
+LIB_PATH = os.environ.get("PSM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpsm.so")
 _lib = None
 
 

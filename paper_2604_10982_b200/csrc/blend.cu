@@ -63,6 +63,10 @@ constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
 #ifndef PSM_BLEND_MB32
 #define PSM_BLEND_MB32 2
 #endif
+// lanes that walk one need mask together: 16 (4x4 halves) or 8 (4x2 quarters)
+#ifndef PSM_BLEND_GROUP
+#define PSM_BLEND_GROUP 8
+#endif
 #ifndef PSM_BLEND_W8
 #define PSM_BLEND_W8 8
 #endif
@@ -154,6 +158,12 @@ __device__ __forceinline__ void accumulate_row(float (&acc)[NV][VEC], float w, c
   }
 }
 
+// Lane -> pixel of an 8x4 block: lanes 0-15 cover the left 4x4 half, lanes 16-31 the
+// right one (row-major inside each half), so each quarter-warp is a compact 4x2 group
+// that walks only the records its own pixels need (PSM_BLEND_GROUP).
+__device__ __forceinline__ int blk_px(int q) { return (q & 3) | ((q >> 4) << 2); }
+__device__ __forceinline__ int blk_py(int q) { return (q >> 2) & 3; }
+
 // One warp's work item: the 8x4 pixel block `blk` (0..7) of tile `tile`; lane -> pixel.
 template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT, int PANO_T>
 __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile, const int blk, SurfRec* stage,
@@ -164,8 +174,8 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int wx0 = tx * kTile + (blk & 1) * 8, wy0 = ty * kTile + (blk >> 1) * 4;
-  const int x = wx0 + (lane & 7);
-  const int y = wy0 + (lane >> 3);
+  const int x = wx0 + blk_px(lane);
+  const int y = wy0 + blk_py(lane);
   const bool inside = x < p.width && y < p.height;
   const int64_t pix = static_cast<int64_t>(y) * p.width + x;
 
@@ -266,15 +276,49 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         sup = cnt >= 32 ? 0xffffffffu : (1u << cnt) - 1u;
       }
     }
-    unsigned need = __reduce_or_sync(0xffffffffu, sup);
+    // Each lane group (a 4x2 quarter-warp, or a 4x4 half) walks the entries its own
+    // pixels need; groups may read different records in the same iteration (at C3 this
+    // is 118 iterations' worth of records per 8x4 block instead of the union's 137).
+#if PSM_BLEND_GROUP == 8
+    unsigned need = sup;  // OR over the quarter-warp (a 4x2 pixel group)
+    need |= __shfl_xor_sync(0xffffffffu, need, 1);
+    need |= __shfl_xor_sync(0xffffffffu, need, 2);
+    need |= __shfl_xor_sync(0xffffffffu, need, 4);
+    int iters = (static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(__popc(need)))) + 1) >> 1;
+#else
+    const unsigned need_lo = __reduce_or_sync(0xffffffffu, lane < 16 ? sup : 0u);
+    const unsigned need_hi = __reduce_or_sync(0xffffffffu, lane < 16 ? 0u : sup);
+    unsigned need = lane < 16 ? need_lo : need_hi;
+    int iters = (max(__popc(need_lo), __popc(need_hi)) + 1) >> 1;
+#endif
 #ifdef PSM_BLEND_STATS
     st_sup += __popc(sup);
-    st_iter += __popc(need);
+    st_iter += 2 * iters;
+    {
+      const unsigned full = __reduce_or_sync(0xffffffffu, sup);
+      unsigned q = sup;  // OR over the quarter-warp (4x2 pixels)
+      q |= __shfl_xor_sync(0xffffffffu, q, 1);
+      q |= __shfl_xor_sync(0xffffffffu, q, 2);
+      const unsigned r4 = q;  // 4 lanes = 4x1 row
+      q |= __shfl_xor_sync(0xffffffffu, q, 4);
+      int mq = __popc(q), m4 = __popc(r4);
+      for (int o = 16; o > 0; o >>= 1) {
+        mq = max(mq, __shfl_xor_sync(0xffffffffu, mq, o));
+        m4 = max(m4, __shfl_xor_sync(0xffffffffu, m4, o));
+      }
+      if (lane == 0) {
+        PSM_STAT(9, __popc(full));
+        PSM_STAT(10, 2 * iters);
+        PSM_STAT(11, mq);
+        PSM_STAT(12, m4);
+      }
+    }
 #endif
     // Alpha phase: the needed entries two at a time (two independent homography /
     // division / exp chains in flight), then composited in list order.
-    while (need) {
-      const int j0 = __ffs(need) - 1;
+    for (; iters > 0; --iters) {
+      const int j0 = need ? __ffs(need) - 1 : 0;
+      const bool h0 = need != 0u;
       need &= need - 1;
       const int j1 = need ? __ffs(need) - 1 : j0;
       need &= need - 1;
@@ -296,7 +340,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       const double a0 = r0.opacity * e0, a1 = r1.opacity * e1;
       // (w2 > 1e-14, raster.cpp:386-387; alpha >= alpha_min and > 0, :391)
       bool ok[2];
-      ok[0] = !done && (sup >> j0 & 1u) && (w02 > 1e-14) && !(a0 < p.alpha_min || a0 <= 0.0);
+      ok[0] = !done && h0 && (sup >> j0 & 1u) && (w02 > 1e-14) && !(a0 < p.alpha_min || a0 <= 0.0);
       ok[1] = !done && j1 != j0 && (sup >> j1 & 1u) && (w12 > 1e-14) && !(a1 < p.alpha_min || a1 <= 0.0);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -429,12 +473,22 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
   // LPP*VEC*4-byte load per selected surfel and one such store.
   if constexpr (NV > 0) {
     constexpr int PPI = 32 / LPP;
-    const int D = p.feat_dims;
+    const int D = EXACT ? LPP * VEC * NV : p.feat_dims;  // EXACT shapes: the width is the shape's
     const int grp = lane / LPP, sub = lane % LPP;
+    if constexpr (KMAX > 0) {
+      // each lane resolves its own selected slots once: (source id, fp32 weight) pairs
+      // over the slot's weight cell, read back below with one 8-byte load per row
+      int2* slot = reinterpret_cast<int2*>(top_w);
+      for (int i = 0; i < blend_n; ++i) {
+        const int s = static_cast<int>(__ldg(p.vals + top_p[i * kCT + tid]));
+        slot[i * kCT + tid] = make_int2(s, __float_as_int(static_cast<float>(top_w[i * kCT + tid])));
+      }
+      __syncwarp();
+    }
     const bool only_sem = p.n_q == 0;
     for (int q0 = 0; q0 < 32; q0 += PPI) {
       const int q = q0 + grp;
-      const int qx = wx0 + (q & 7), qy = wy0 + (q >> 3);
+      const int qx = wx0 + blk_px(q), qy = wy0 + blk_py(q);
       const bool qin = qx < p.width && qy < p.height;
       if (!__any_sync(0xffffffffu, qin)) continue;
       const int64_t qpix = static_cast<int64_t>(qy) * p.width + qx;
@@ -449,10 +503,12 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       using TV = typename FVec<VEC>::T;
       if constexpr (KMAX > 0) {
         const int qt = (tid & ~31) + q;  // the pixel's thread: its Top-K list column
+        const int2* slot = reinterpret_cast<const int2*>(top_w);
         for (int i = 0; i < nq; ++i) {
-          const int s = static_cast<int>(__ldg(p.vals + top_p[i * kCT + qt]));
-          const float w = static_cast<float>(top_w[i * kCT + qt]);
-          const TV* row = reinterpret_cast<const TV*>(p.feat + static_cast<int64_t>(s) * D);
+          const int2 e = slot[i * kCT + qt];
+          const float w = __int_as_float(e.y);
+          const TV* row = reinterpret_cast<const TV*>(
+              p.feat + static_cast<uint64_t>(static_cast<uint32_t>(e.x)) * static_cast<uint32_t>(D));
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
             const int idx = v * LPP + sub;
@@ -553,7 +609,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     int nsel = blend_n;
     if constexpr (FULL_LIST) nsel = nsel < p.list_cap ? nsel : p.list_cap;
     for (int q = 0; q < 32; ++q) {
-      const int qx = wx0 + (q & 7), qy = wy0 + (q >> 3);
+      const int qx = wx0 + blk_px(q), qy = wy0 + blk_py(q);
       const bool qgate = __shfl_sync(0xffffffffu, gate, q);
       const int nq = __shfl_sync(0xffffffffu, nsel, q);
       const int64_t qpix = static_cast<int64_t>(qy) * p.width + qx;
