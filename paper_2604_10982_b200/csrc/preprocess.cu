@@ -174,7 +174,10 @@ __device__ __forceinline__ bool project_one(int64_t i, const double* __restrict_
   return true;
 }
 
-__global__ void __launch_bounds__(256, 3) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
+#ifndef PSM_PRE_MINB
+#define PSM_PRE_MINB 3
+#endif
+__global__ void __launch_bounds__(256, PSM_PRE_MINB) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
                                                           DevCamera cam, DevRaster rs, SurfRec* __restrict__ recs,
                                                           BinRec* __restrict__ bins,
                                                           uint64_t* __restrict__ depth_bits,

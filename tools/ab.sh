@@ -9,6 +9,6 @@ for r in $(seq 1 $rounds); do
     PSM_LIB_PATH=$lib timeout 300 python bench.py --workload $wl --no-cpu-baseline --steps 30 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1]); s=d['config']['stage_ms']
-print('$v', round(d['value'],1), 'blend', round(s['blend'],4), 'total', round(s['total'],4), 'pre', round(s['preprocess'],4), 'emit', round(s['emit'],4), 'sort', round(s['tile_sort'],4))"
+print('$v', round(d['value'],1), 'blend', round(s['blend'],4), 'total', round(s['total'],4), 'pre', round(s['preprocess'],4), 'emit', round(s['emit'],4), 'sort', round(s['tile_sort'],4), 'e2e', round(d['e2e']['value'],1) if d.get('e2e') else None)"
   done
 done
