@@ -171,10 +171,13 @@ int check_config(psm_ctx* ctx, const psm_raster_config* cfg, int feat_dims) {
 // on_band(band, y0, y1) is called after each band's launch (it queues that band's
 // device-to-host copies on the copy stream, overlapping the next band's blend).
 using BandHook = std::function<int(int band, int y0, int y1)>;
-#ifndef PSM_HOST_BANDS
-#define PSM_HOST_BANDS 8
+// cumulative band ends in 64ths of the tile rows; <= 8 bands (band events, work counters
+// small[8..16))
+// (C3 e2e, measured: 4,12,64 -> 180 frames/s; eight equal bands 174; 3,10,24,64 179;
+// 2,8,64 171)
+#ifndef PSM_HOST_BAND_CUTS
+#define PSM_HOST_BAND_CUTS 4, 12, 64
 #endif
-constexpr int kHostBands = PSM_HOST_BANDS;  // <= 8 (band events, work counters small[8..16))
 
 int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
                 const Planes& pl, psm_debug* dbg, const BandHook* on_band = nullptr) {
@@ -351,9 +354,18 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     launch_blend(bp, tiles, topk, st);
     PSM_CUDA_TRY(cudaGetLastError());
   } else {
-    const int bands = tiles_y < kHostBands ? tiles_y : kHostBands;
-    for (int b = 0; b < bands; ++b) {
-      const int ty0 = tiles_y * b / bands, ty1 = tiles_y * (b + 1) / bands;
+    // Band b ends at kBandCuts[b]/64 of the tile rows. Host-target frames are bound by the
+    // copies (PCIe), so the first band is small (its copies start soon after the front end)
+    // and the rest are few and large (every copy costs ~4 us on the copy engine).
+    static constexpr int kBandCuts[] = {PSM_HOST_BAND_CUTS};
+    constexpr int n_cuts = static_cast<int>(sizeof(kBandCuts) / sizeof(kBandCuts[0]));
+    static_assert(n_cuts <= 8 && kBandCuts[n_cuts - 1] == 64, "band cuts: <= 8 bands, the last at 64/64");
+    int ty1 = 0;
+    for (int b = 0; b < n_cuts && ty1 < tiles_y; ++b) {
+      const int ty0 = ty1;
+      ty1 = (tiles_y * kBandCuts[b] + 63) / 64;
+      if (ty1 <= ty0) ty1 = ty0 + 1;
+      if (ty1 > tiles_y || b == n_cuts - 1) ty1 = tiles_y;
       bp.tile_base = ty0 * tiles_x;
       bp.work = reinterpret_cast<int32_t*>(small + 8 + b);
       launch_blend(bp, (ty1 - ty0) * tiles_x, topk, st);
