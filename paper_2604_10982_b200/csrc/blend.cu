@@ -63,9 +63,14 @@ constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
 #ifndef PSM_BLEND_MB32
 #define PSM_BLEND_MB32 2
 #endif
-// lanes that walk one need mask together: 16 (4x4 halves) or 8 (4x2 quarters)
+// candidate records per alpha-phase iteration (independent fp64 chains in flight)
+#ifndef PSM_BLEND_PER
+#define PSM_BLEND_PER 1
+#endif
+// lanes that walk one need mask together: 1, 2 (the default: two horizontally adjacent
+// pixels), 4 (a 4x1 row), 8 (4x2) or 16 (4x4). C3 blend: 0.812 / 0.809 / 0.834 / 0.841 / 0.875 ms
 #ifndef PSM_BLEND_GROUP
-#define PSM_BLEND_GROUP 8
+#define PSM_BLEND_GROUP 2
 #endif
 #ifndef PSM_BLEND_W8
 #define PSM_BLEND_W8 8
@@ -159,8 +164,8 @@ __device__ __forceinline__ void accumulate_row(float (&acc)[NV][VEC], float w, c
 }
 
 // Lane -> pixel of an 8x4 block: lanes 0-15 cover the left 4x4 half, lanes 16-31 the
-// right one (row-major inside each half), so each quarter-warp is a compact 4x2 group
-// that walks only the records its own pixels need (PSM_BLEND_GROUP).
+// right one (row-major inside each half), so aligned lane groups of 2, 4, 8 and 16 are
+// compact pixel groups that walk only the records their own pixels need (PSM_BLEND_GROUP).
 __device__ __forceinline__ int blk_px(int q) { return (q & 3) | ((q >> 4) << 2); }
 __device__ __forceinline__ int blk_py(int q) { return (q >> 2) & 3; }
 
@@ -170,6 +175,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
                                             const uint64_t* exp_tab, double* top_w, int* top_p) {
   constexpr int kChunk = chunk_for(KMAX);
   constexpr int kCT = cta_threads(KMAX);  // Top-K column stride
+  constexpr int kPer = PSM_BLEND_PER;     // candidate records evaluated per iteration
   const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -276,24 +282,24 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         sup = cnt >= 32 ? 0xffffffffu : (1u << cnt) - 1u;
       }
     }
-    // Each lane group (a 4x2 quarter-warp, or a 4x4 half) walks the entries its own
-    // pixels need; groups may read different records in the same iteration (at C3 this
-    // is 118 iterations' worth of records per 8x4 block instead of the union's 137).
-#if PSM_BLEND_GROUP == 8
-    unsigned need = sup;  // OR over the quarter-warp (a 4x2 pixel group)
-    need |= __shfl_xor_sync(0xffffffffu, need, 1);
-    need |= __shfl_xor_sync(0xffffffffu, need, 2);
-    need |= __shfl_xor_sync(0xffffffffu, need, 4);
-    int iters = (static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(__popc(need)))) + 1) >> 1;
+    // Each lane group (PSM_BLEND_GROUP lanes) walks the entries its own pixels need, one
+    // per iteration; groups read different staged records in the same iteration (the
+    // warp iterates max over groups instead of the union of the block's needs: at C3 the
+    // union is 137 records per 8x4 block, a 4x2 group's maximum 118, a 4x1 row's 115).
+#if PSM_BLEND_GROUP <= 8
+    unsigned need = sup;  // OR over the lane group (8 lanes: a 4x2 pixel group; 4: a 4x1 row)
+#pragma unroll
+    for (int o = 1; o < PSM_BLEND_GROUP; o <<= 1) need |= __shfl_xor_sync(0xffffffffu, need, o);
+    int iters = (static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(__popc(need)))) + kPer - 1) / kPer;
 #else
     const unsigned need_lo = __reduce_or_sync(0xffffffffu, lane < 16 ? sup : 0u);
     const unsigned need_hi = __reduce_or_sync(0xffffffffu, lane < 16 ? 0u : sup);
     unsigned need = lane < 16 ? need_lo : need_hi;
-    int iters = (max(__popc(need_lo), __popc(need_hi)) + 1) >> 1;
+    int iters = (max(__popc(need_lo), __popc(need_hi)) + kPer - 1) / kPer;
 #endif
 #ifdef PSM_BLEND_STATS
     st_sup += __popc(sup);
-    st_iter += 2 * iters;
+    st_iter += kPer * iters;
     {
       const unsigned full = __reduce_or_sync(0xffffffffu, sup);
       unsigned q = sup;  // OR over the quarter-warp (4x2 pixels)
@@ -308,47 +314,57 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       }
       if (lane == 0) {
         PSM_STAT(9, __popc(full));
-        PSM_STAT(10, 2 * iters);
+        PSM_STAT(10, kPer * iters);
         PSM_STAT(11, mq);
         PSM_STAT(12, m4);
       }
     }
 #endif
-    // Alpha phase: the needed entries two at a time (two independent homography /
-    // division / exp chains in flight), then composited in list order.
+    // Alpha phase: the needed entries kPer at a time (independent homography / division /
+    // exp chains in flight), then composited in list order.
     for (; iters > 0; --iters) {
-      const int j0 = need ? __ffs(need) - 1 : 0;
-      const bool h0 = need != 0u;
-      need &= need - 1;
-      const int j1 = need ? __ffs(need) - 1 : j0;
-      need &= need - 1;
-      const SurfRec& r0 = recs[j0];
-      const SurfRec& r1 = recs[j1];
-      const double w00 = r0.h[0] * rx + r0.h[1] * ry + r0.h[2];
-      const double w01 = r0.h[3] * rx + r0.h[4] * ry + r0.h[5];
-      const double w02 = r0.h[6] * rx + r0.h[7] * ry + r0.h[8];
-      const double w10 = r1.h[0] * rx + r1.h[1] * ry + r1.h[2];
-      const double w11 = r1.h[3] * rx + r1.h[4] * ry + r1.h[5];
-      const double w12 = r1.h[6] * rx + r1.h[7] * ry + r1.h[8];
-      const double rcp0 = 1.0 / w02, rcp1 = 1.0 / w12;
-      const double u0 = w00 * rcp0, v0 = w01 * rcp0;
-      const double u1 = w10 * rcp1, v1 = w11 * rcp1;
-      const double x0 = -0.5 * (u0 * u0 + v0 * v0), x1 = -0.5 * (u1 * u1 + v1 * v1);
-      double e0 = psm_exp_main(x0, exp_tab), e1 = psm_exp_main(x1, exp_tab);
-      if (!psm_exp_main_ok(x0)) e0 = psm_exp_t(x0, exp_tab);
-      if (!psm_exp_main_ok(x1)) e1 = psm_exp_t(x1, exp_tab);
-      const double a0 = r0.opacity * e0, a1 = r1.opacity * e1;
-      // (w2 > 1e-14, raster.cpp:386-387; alpha >= alpha_min and > 0, :391)
-      bool ok[2];
-      ok[0] = !done && h0 && (sup >> j0 & 1u) && (w02 > 1e-14) && !(a0 < p.alpha_min || a0 <= 0.0);
-      ok[1] = !done && j1 != j0 && (sup >> j1 & 1u) && (w12 > 1e-14) && !(a1 < p.alpha_min || a1 <= 0.0);
+      int jj[kPer];
+      bool hh[kPer];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < kPer; ++c) {
+        hh[c] = need != 0u;
+        jj[c] = hh[c] ? __ffs(need) - 1 : 0;
+        need &= need - 1;
+      }
+      double al[kPer], rc[kPer], xs[kPer];
+      bool ok[kPer];
+      bool main_ok = true;
+#pragma unroll
+      for (int c = 0; c < kPer; ++c) {
+        const SurfRec& r = recs[jj[c]];
+        const double w0 = r.h[0] * rx + r.h[1] * ry + r.h[2];
+        const double w1 = r.h[3] * rx + r.h[4] * ry + r.h[5];
+        const double w2 = r.h[6] * rx + r.h[7] * ry + r.h[8];
+        rc[c] = 1.0 / w2;
+        const double u = w0 * rc[c], v = w1 * rc[c];
+        xs[c] = -0.5 * (u * u + v * v);
+        al[c] = psm_exp_main(xs[c], exp_tab);
+        main_ok = main_ok && psm_exp_main_ok(xs[c]);
+        // (w2 > 1e-14, raster.cpp:386-387)
+        ok[c] = !done && hh[c] && (sup >> jj[c] & 1u) && (w2 > 1e-14);
+      }
+      if (!main_ok) {  // one branch for the rare special ranges of every chain
+#pragma unroll
+        for (int c = 0; c < kPer; ++c)
+          if (!psm_exp_main_ok(xs[c])) al[c] = psm_exp_t(xs[c], exp_tab);
+      }
+#pragma unroll
+      for (int c = 0; c < kPer; ++c) {
+        al[c] = recs[jj[c]].opacity * al[c];
+        ok[c] = ok[c] && !(al[c] < p.alpha_min || al[c] <= 0.0);  // raster.cpp:391
+      }
+#pragma unroll
+      for (int c = 0; c < kPer; ++c) {
         if (!ok[c] || done) continue;
-        const SurfRec& r = c ? r1 : r0;
-        const double alpha = c ? a1 : a0;
-        const double rcp = c ? rcp1 : rcp0;
-        const int j = c ? j1 : j0;
+        const SurfRec& r = recs[jj[c]];
+        const double alpha = al[c];
+        const double rcp = rc[c];
+        const int j = jj[c];
 #ifdef PSM_BLEND_STATS
         st_alpha++;
 #endif
