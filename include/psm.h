@@ -128,8 +128,10 @@ typedef struct psm_debug {
   int32_t* topk_src;
 } psm_debug;
 
-/* Stage timings of the last render when profiling is on (CUDA events on the
- * context stream), milliseconds. */
+/* Stage timings of the last synchronised render when profiling is on (CUDA events
+ * on the context stream), milliseconds. Profiling does not make a device-target
+ * render synchronous: the times are read when the frame is synchronised (psm_sync,
+ * or a render that returns counters or host planes). */
 typedef struct psm_stage_times {
   float preprocess;   /* K1: project_surfel, hot records, box, per-tile bucket sizes (raster.cpp:94-142,321-353,59-74) */
   float tile_scan;    /* K3: bucket offsets = per-tile ranges, RN-Total (raster.cpp:84-88) */

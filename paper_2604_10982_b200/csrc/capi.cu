@@ -215,37 +215,38 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   uint32_t* rn_dev = reinterpret_cast<uint32_t*>(small + 5);
   uint32_t* rn_eff_dev = reinterpret_cast<uint32_t*>(small + 6);
   int32_t* key_ovf = reinterpret_cast<int32_t*>(small + 7);
-  PSM_CUDA_TRY(cudaMemsetAsync(small, 0, 16 * sizeof(unsigned long long), st));
   int32_t* ranges = nullptr;
   PSM_TRY(ensure(ctx, ctx->ranges, static_cast<size_t>(tiles) * 2, &ranges));
-  PSM_CUDA_TRY(cudaMemsetAsync(ranges, 0, sizeof(int32_t) * 2 * tiles, st));
+  uint32_t* tcounts = nullptr;
+  unsigned long long* dminmax = nullptr;
+  if (n > 0) {
+    PSM_TRY(ensure(ctx, ctx->tile_counts, static_cast<size_t>(tiles) * kSplit, &tcounts));
+    PSM_TRY(ensure(ctx, ctx->dminmax, 2, &dminmax));
+  }
 
   ctx->ev_next = 0;
   record(ctx, 0);
+  // counters, ranges, tile counters and the depth range reset in one launch
+  launch_frame_init(small, ranges, 2 * tiles, tcounts, n > 0 ? tiles * kSplit : 0, dminmax, st);
+  PSM_CUDA_TRY(cudaGetLastError());
   uint32_t* tvals_s = nullptr;
   uint8_t* tmasks_s = nullptr;
   const int32_t* tclasses_s = nullptr;
   int64_t key_cap = 0;
   if (n > 0) {
     SurfRec* recs; BinRec* bins; uint64_t* dbits; int32_t* valid;
-    uint32_t *tcounts, *cursor, *ttotals, *tstart;
+    uint32_t *cursor, *ttotals, *tstart;
     int32_t* tclasses;
     PSM_TRY(ensure(ctx, ctx->recs, n, &recs));
     PSM_TRY(ensure(ctx, ctx->bins, n, &bins));
     PSM_TRY(ensure(ctx, ctx->depth_bits, n, &dbits));
     PSM_TRY(ensure(ctx, ctx->valid, n, &valid));
-    PSM_TRY(ensure(ctx, ctx->tile_counts, static_cast<size_t>(tiles) * kSplit, &tcounts));
     PSM_TRY(ensure(ctx, ctx->cursor, static_cast<size_t>(tiles) * kSplit, &cursor));
     PSM_TRY(ensure(ctx, ctx->tile_totals, tiles, &ttotals));
     PSM_TRY(ensure(ctx, ctx->tile_start, tiles, &tstart));
     // K3b's sort-class lists and counts, and the blend's heaviest-first tile order
     PSM_TRY(ensure(ctx, ctx->tclasses, static_cast<size_t>(tiles) * (psm::kSortClasses + 2), &tclasses));
-    PSM_CUDA_TRY(cudaMemsetAsync(tcounts, 0, sizeof(uint32_t) * tiles * kSplit, st));
     // K1: projection, records, per-tile bucket sizes
-    unsigned long long* dminmax;
-    PSM_TRY(ensure(ctx, ctx->dminmax, 2, &dminmax));
-    const unsigned long long init_minmax[2] = {~0ull, 0ull};
-    PSM_CUDA_TRY(cudaMemcpyAsync(dminmax, init_minmax, sizeof init_minmax, cudaMemcpyHostToDevice, st));
     launch_preprocess(sc->surfels, n, dc, rs, recs, bins, dbits, tcounts, valid, n_proj_dev, dminmax,
                       reinterpret_cast<int32_t*>(small), st);
     PSM_CUDA_TRY(cudaGetLastError());
@@ -561,7 +562,7 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
   };
   const BandHook* hook = host_out ? &band_d2h : nullptr;
   PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg, hook));
-  if (counters || host_out || ctx->profiling || dbg) {
+  if (counters || host_out || dbg) {
     for (int attempt = 0;; ++attempt) {
       PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
       bool rerun = false;

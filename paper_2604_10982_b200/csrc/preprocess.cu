@@ -224,7 +224,28 @@ __global__ void __launch_bounds__(256, PSM_PRE_MINB) preprocess_kernel(const dou
   }
 }
 
+// Per-frame reset in one launch (instead of three memsets and a host-to-device copy):
+// the 16 frame counters, the per-tile ranges, the split tile counters, and the depth
+// range's (min, max) identities.
+__global__ void frame_init_kernel(unsigned long long* __restrict__ small, int32_t* __restrict__ ranges, int n_ranges,
+                                  uint32_t* __restrict__ tcounts, int n_counts,
+                                  unsigned long long* __restrict__ dminmax) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  if (t < 16) small[t] = 0ull;
+  if (dminmax && t < 2) dminmax[t] = t == 0 ? ~0ull : 0ull;
+  for (int i = t; i < n_ranges; i += stride) ranges[i] = 0;
+  for (int i = t; i < n_counts; i += stride) tcounts[i] = 0u;
+}
+
 }  // namespace
+
+void launch_frame_init(unsigned long long* small, int32_t* ranges, int n_ranges, uint32_t* tcounts, int n_counts,
+                       unsigned long long* dminmax, cudaStream_t stream) {
+  const int work = n_ranges > n_counts ? n_ranges : n_counts;
+  int blocks = (work + 255) / 256;
+  blocks = blocks < 1 ? 1 : (blocks > 1184 ? 1184 : blocks);
+  frame_init_kernel<<<blocks, 256, 0, stream>>>(small, ranges, n_ranges, tcounts, n_counts, dminmax);
+}
 
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
                        BinRec* bins, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,

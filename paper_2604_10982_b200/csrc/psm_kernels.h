@@ -86,6 +86,8 @@ struct LabelParams {
 void launch_assign_labels(const LabelParams& p, cudaStream_t st);
 
 // K1 preprocess.cu
+void launch_frame_init(unsigned long long* small, int32_t* ranges, int n_ranges, uint32_t* tcounts, int n_counts,
+                       unsigned long long* dminmax, cudaStream_t stream);
 void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam, const DevRaster& rs, SurfRec* recs,
                        BinRec* bins, uint64_t* depth_bits, uint32_t* tile_counts, int32_t* valid,
                        uint32_t* n_proj, unsigned long long* depth_minmax, int32_t* err, cudaStream_t stream);
