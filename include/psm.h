@@ -162,7 +162,9 @@ int psm_scene_free(psm_ctx* ctx, psm_scene* scene);
 int psm_scene_info(const psm_scene* scene, int64_t* n, int32_t* c_sem, int32_t* n_q);
 
 /* render_into (raster.cpp:273-511). counters may be NULL. With on_device
- * targets and counters == NULL the call is asynchronous. */
+ * targets and counters == NULL the call is asynchronous: psm_sync waits for every
+ * asynchronous frame since the last synchronisation, checks each one's counters and
+ * re-renders, in order, from the first that outgrew the context's buffers. */
 int psm_render(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam,
                const psm_raster_config* cfg, const psm_targets* targets, psm_counters* counters);
 
@@ -172,7 +174,13 @@ int psm_render_debug(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam
                      psm_counters* counters, psm_debug* debug);
 
 /* n_views independent renders (one per camera) into n_views target sets;
- * views share the scene upload. counters may be NULL or an array of n_views. */
+ * views share the scene upload. counters may be NULL or an array of n_views.
+ * With device targets and counters == NULL the batch is asynchronous and pipelined:
+ * views alternate between the context and an internal second context on a second
+ * stream (one view's front end overlaps the other's blend); later work on the
+ * context's stream is ordered after every view, and psm_sync validates them all
+ * (psm_last_counters then holds the last view's counters). Views of different
+ * parity (rendered by different contexts) must not share target planes. */
 int psm_render_batch(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cams, int32_t n_views,
                      const psm_raster_config* cfg, const psm_targets* targets,
                      psm_counters* counters);

@@ -77,14 +77,29 @@ struct psm_ctx {
   int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
   int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
   psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
-  int64_t* h_small = nullptr;  // pinned: counters read-back
-  // last asynchronous frame (device targets, no counters): checked, and re-rendered if it
-  // outgrew its buffers, by psm_sync
-  bool pend_valid = false;
-  const psm_scene* pend_scene = nullptr;
-  psm_camera pend_cam{};
-  psm_raster_config pend_cfg{};
-  psm::Planes pend_pl{};
+  // Pinned counter read-back: one 8-slot record per pending asynchronous frame plus one
+  // for synchronous frames (h_ring[kMaxPend]); h_small points at the current frame's.
+  static constexpr int kMaxPend = 64;
+  int64_t* h_ring = nullptr;
+  int64_t* h_small = nullptr;
+  // Asynchronous frames (device targets, no counters) not yet validated: psm_sync checks
+  // each one's counters in order and, from the first that outgrew its buffers, re-renders
+  // it and every later one (so planes shared between pending frames end as the last wrote
+  // them). A synchronous frame, or a full list, drains the list first.
+  struct Pending {
+    const psm_scene* scene;
+    psm_camera cam;
+    psm_raster_config cfg;
+    psm::Planes pl;
+  };
+  std::vector<Pending> pend;
+  // psm_render_batch: a second context (own stream and scratch) that renders every other
+  // view, so one view's front end overlaps the other's blend and the small latency-bound
+  // launches interleave; created on first use, joined back into `stream` after the batch.
+  psm_ctx* twin = nullptr;
+  cudaEvent_t batch_fork = nullptr, batch_join = nullptr;
+  bool twin_pending = false;  // the twin rendered views not yet validated (psm_sync drains it)
+  bool twin_last = false;     // ... including the batch's last view (its counters are the last)
 };
 
 namespace psm {
@@ -468,6 +483,18 @@ void read_times(psm_ctx* ctx) {
   cudaEventElapsedTime(&ctx->times.total, ctx->ev[0], ctx->ev[5]);
 }
 
+int sync_impl(psm_ctx* ctx);
+
+// Validates (and if needed re-renders) the views the twin context rendered in the last
+// batch; after it the twin's frames are complete in stream order before ctx's next work.
+int drain_twin(psm_ctx* ctx) {
+  if (!ctx->twin_pending) return PSM_OK;
+  ctx->twin_pending = false;
+  const int st = sync_impl(ctx->twin);
+  if (st != PSM_OK) return fail(ctx, st, std::string("batch view: ") + ctx->twin->err);
+  return PSM_OK;
+}
+
 // pt != NULL: render_panoptic. The standard planes then live in context scratch, the
 // feature planes are not materialised, and pt's three id planes are the outputs.
 int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
@@ -561,8 +588,14 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
     return PSM_OK;
   };
   const BandHook* hook = host_out ? &band_d2h : nullptr;
+  // earlier asynchronous frames are validated before a synchronous one, or when the list is full
+  const bool async = !(counters || host_out || dbg);
+  if (!async) PSM_TRY(drain_twin(ctx));
+  if (!ctx->pend.empty() && (!async || ctx->pend.size() >= static_cast<size_t>(psm_ctx::kMaxPend)))
+    PSM_TRY(sync_impl(ctx));
+  ctx->h_small = ctx->h_ring + 8 * (async ? ctx->pend.size() : static_cast<size_t>(psm_ctx::kMaxPend));
   PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg, hook));
-  if (counters || host_out || dbg) {
+  if (!async) {
     for (int attempt = 0;; ++attempt) {
       PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
       bool rerun = false;
@@ -571,16 +604,11 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
       if (attempt >= 3) return fail(ctx, PSM_ENOMEM, "render buffers did not converge");
       PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, dbg, hook));
     }
-    ctx->pend_valid = false;
     finish_counters(ctx);
     read_times(ctx);
     if (counters) *counters = ctx->last;
   } else {
-    ctx->pend_valid = true;
-    ctx->pend_scene = sc;
-    ctx->pend_cam = *cam;
-    ctx->pend_cfg = *cfg;
-    ctx->pend_pl = pl;
+    ctx->pend.push_back({sc, *cam, *cfg, pl});
   }
   return PSM_OK;
 }
@@ -589,16 +617,29 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
 int sync_impl(psm_ctx* ctx) {
   PSM_CUDA_TRY(cudaSetDevice(ctx->device));
   PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  if (ctx->pend_valid) {
-    for (int attempt = 0;; ++attempt) {
+  if (!ctx->pend.empty()) {
+    std::vector<psm_ctx::Pending> pend;
+    pend.swap(ctx->pend);  // the list is consumed whatever the outcome
+    size_t first = pend.size();
+    for (size_t j = 0; j < pend.size(); ++j) {  // every frame's flags (errors, capacities)
+      ctx->h_small = ctx->h_ring + 8 * j;
       bool rerun = false;
       PSM_TRY(check_frame(ctx, &rerun));
-      if (!rerun) break;
-      if (attempt >= 3) return fail(ctx, PSM_ENOMEM, "render buffers did not converge");
-      PSM_TRY(render_impl(ctx, ctx->pend_scene, &ctx->pend_cam, &ctx->pend_cfg, ctx->pend_pl, nullptr));
-      PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      if (rerun && first == pend.size()) first = j;
     }
-    ctx->pend_valid = false;
+    ctx->h_small = ctx->h_ring + 8 * psm_ctx::kMaxPend;
+    for (size_t j = first; j < pend.size(); ++j) {  // re-render in the original order
+      const psm_ctx::Pending& f = pend[j];
+      for (int attempt = 0;; ++attempt) {
+        PSM_TRY(render_impl(ctx, f.scene, &f.cam, &f.cfg, f.pl, nullptr));
+        PSM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        bool rerun = false;
+        PSM_TRY(check_frame(ctx, &rerun));
+        if (!rerun) break;
+        if (attempt >= 3) return fail(ctx, PSM_ENOMEM, "render buffers did not converge");
+      }
+    }
+    if (first == pend.size()) ctx->h_small = ctx->h_ring + 8 * (pend.size() - 1);  // the last frame's counters
   }
   finish_counters(ctx);
   read_times(ctx);
@@ -646,8 +687,10 @@ int psm_create(int device, void* stream, psm_ctx** out) {
   }
   for (auto& e : ctx->band_ev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { delete ctx; return PSM_ECUDA; }
-  if (cudaMallocHost(&ctx->h_small, 8 * sizeof(int64_t)) != cudaSuccess) { delete ctx; return PSM_ENOMEM; }
-  std::memset(ctx->h_small, 0, 8 * sizeof(int64_t));
+  const size_t ring_bytes = 8 * sizeof(int64_t) * (psm_ctx::kMaxPend + 1);
+  if (cudaMallocHost(&ctx->h_ring, ring_bytes) != cudaSuccess) { delete ctx; return PSM_ENOMEM; }
+  std::memset(ctx->h_ring, 0, ring_bytes);
+  ctx->h_small = ctx->h_ring + 8 * psm_ctx::kMaxPend;
   *out = ctx;
   return PSM_OK;
 }
@@ -675,7 +718,10 @@ int psm_destroy(psm_ctx* ctx) {
   for (auto& e : ctx->band_ev) if (e) cudaEventDestroy(e);
   if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
-  if (ctx->h_small) cudaFreeHost(ctx->h_small);
+  if (ctx->h_ring) cudaFreeHost(ctx->h_ring);
+  if (ctx->twin) psm_destroy(ctx->twin);
+  if (ctx->batch_fork) cudaEventDestroy(ctx->batch_fork);
+  if (ctx->batch_join) cudaEventDestroy(ctx->batch_join);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PSM_OK;
@@ -697,7 +743,11 @@ int psm_get_stage_times(const psm_ctx* ctx, psm_stage_times* out) {
 
 int psm_sync(psm_ctx* ctx) {
   if (!ctx) return PSM_EINVAL;
-  return psm::sync_impl(ctx);
+  const bool twin_last = ctx->twin_pending && ctx->twin_last;
+  PSM_TRY(psm::drain_twin(ctx));  // views of the last batch rendered by the twin context
+  PSM_TRY(psm::sync_impl(ctx));
+  if (twin_last) ctx->last = ctx->twin->last;  // psm_last_counters: the batch's last view
+  return PSM_OK;
 }
 
 int psm_last_counters(const psm_ctx* ctx, psm_counters* out) {
@@ -897,6 +947,9 @@ int psm_render_backward(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam
   pl.ins = nullptr;
   pl.cache = true;
   if (ctx->list_cap == 0) ctx->list_cap = 128;
+  PSM_TRY(psm::drain_twin(ctx));  // validate earlier asynchronous frames first
+  if (!ctx->pend.empty()) PSM_TRY(psm::sync_impl(ctx));
+  ctx->h_small = ctx->h_ring + 8 * psm_ctx::kMaxPend;
   for (int attempt = 0;; ++attempt) {
     PSM_TRY(psm::render_impl(ctx, sc, cam, cfg, pl, nullptr));
     PSM_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1014,10 +1067,38 @@ int psm_render_debug(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam
 int psm_render_batch(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cams, int32_t n_views,
                      const psm_raster_config* cfg, const psm_targets* targets, psm_counters* counters) {
   if (!ctx || !cams || !targets || n_views < 0) return PSM_EINVAL;
-  for (int32_t v = 0; v < n_views; ++v) {
-    const int st = psm_render(ctx, scene, cams + v, cfg, targets + v, counters ? counters + v : nullptr);
-    if (st != PSM_OK) return st;
+  bool pipelined = !counters && n_views >= 2;
+  for (int32_t v = 0; v < n_views && pipelined; ++v) pipelined = targets[v].on_device != 0;
+  if (!pipelined) {  // counters or host planes: every view synchronises anyway
+    for (int32_t v = 0; v < n_views; ++v) {
+      const int st = psm_render(ctx, scene, cams + v, cfg, targets + v, counters ? counters + v : nullptr);
+      if (st != PSM_OK) return st;
+    }
+    return PSM_OK;
   }
+  // device targets, no counters: views alternate between this context and its twin on two
+  // streams (asynchronous, like psm_render; psm_sync validates both contexts' frames)
+  // earlier unvalidated frames first: a re-render after this batch could overwrite its planes
+  if (ctx->twin_pending || !ctx->pend.empty()) PSM_TRY(psm_sync(ctx));
+  PSM_CUDA_TRY(cudaSetDevice(ctx->device));
+  if (!ctx->twin) {
+    PSM_TRY(psm_create(ctx->device, nullptr, &ctx->twin));
+    PSM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->batch_fork, cudaEventDisableTiming));
+    PSM_CUDA_TRY(cudaEventCreateWithFlags(&ctx->batch_join, cudaEventDisableTiming));
+  }
+  psm_ctx* tw = ctx->twin;
+  tw->profiling = ctx->profiling;
+  PSM_CUDA_TRY(cudaEventRecord(ctx->batch_fork, ctx->stream));  // the twin starts after earlier work
+  PSM_CUDA_TRY(cudaStreamWaitEvent(tw->stream, ctx->batch_fork, 0));
+  for (int32_t v = 0; v < n_views; ++v) {
+    psm_ctx* c = (v & 1) ? tw : ctx;
+    const int st = psm_render(c, scene, cams + v, cfg, targets + v, nullptr);
+    if (st != PSM_OK) return c == ctx ? st : fail(ctx, st, std::string("batch view: ") + tw->err);
+  }
+  ctx->twin_pending = true;
+  ctx->twin_last = (n_views & 1) == 0;
+  PSM_CUDA_TRY(cudaEventRecord(ctx->batch_join, tw->stream));  // later work on ctx->stream sees every view
+  PSM_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->batch_join, 0));
   return PSM_OK;
 }
 

@@ -16,7 +16,7 @@ import ctypes as C
 import enum
 import math
 from dataclasses import dataclass, field
-from typing import Tuple, List, Optional
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -370,6 +370,23 @@ class Renderer:
                             C.byref(cnt) if counters else None)
         _check(st, self.ctx, "render")
         return cnt if counters else None
+
+    def render_batch_device(self, dscene: DeviceScene, cams: Sequence[Camera], cfg: RasterConfig,
+                            planes: Sequence[dict]) -> None:
+        """psm_render_batch into device planes (one {name: device pointer} dict per view, as
+        render_device): asynchronous and pipelined over two streams; psm_sync (`sync`) validates."""
+        lib = _lib.load()
+        n = len(cams)
+        if len(planes) != n:
+            raise ValueError("one plane set per camera")
+        tg = (A.psm_targets * max(n, 1))()
+        for i, pl in enumerate(planes):
+            tg[i] = A.psm_targets(*(pl.get(k) for k in ("color", "depth", "normal", "sem_feat", "ins_dist",
+                                                        "ins_argmax", "alpha_acc", "blend_count")), 1)
+        cc = (A.psm_camera * max(n, 1))(*(c.to_c() for c in cams))
+        c_cfg = cfg.to_c()
+        _check(lib.psm_render_batch(self.ctx, dscene.handle, cc, n, C.byref(c_cfg), tg, None), self.ctx,
+               "render_batch")
 
     def render_backward(self, scene, labels, cam: Camera, cfg: RasterConfig, g_color=None, g_sem=None,
                         g_ins=None) -> dict:
