@@ -242,7 +242,10 @@ struct EmitItem {
 };
 constexpr int kEmitWarps = 8;
 
-__global__ void __launch_bounds__(32 * kEmitWarps) emit_kernel(const int32_t* __restrict__ valid, int64_t n,
+#ifndef PSM_EMIT_MINB
+#define PSM_EMIT_MINB 4
+#endif
+__global__ void __launch_bounds__(32 * kEmitWarps, PSM_EMIT_MINB) emit_kernel(const int32_t* __restrict__ valid, int64_t n,
                                                    const SurfRec* __restrict__ recs, const BinRec* __restrict__ bins,
                                                    DevRaster rs, int img_h, uint32_t* __restrict__ cursor,
                                                    const uint32_t* __restrict__ tile_start, uint32_t cap,
