@@ -53,8 +53,10 @@ def launches(csv_in, out):
     h = rows[0]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     rows = [r for r in rows[1:] if len(r) > vi]
-    starts = [i for i, r in enumerate(rows) if "preprocess_kernel" in r[ki]]
-    if starts:  # keep the last frame (from its preprocess launch; memsets are not kernels)
+    starts = [i for i, r in enumerate(rows) if "frame_init_kernel" in r[ki]]
+    if not starts:  # captures before the one-kernel frame reset started at preprocess
+        starts = [i for i, r in enumerate(rows) if "preprocess_kernel" in r[ki]]
+    if starts:  # keep the last frame (from its first launch; memsets are not kernels)
         rows = rows[starts[-1]:]
     agg = {}
     for r in rows:
