@@ -16,10 +16,11 @@
 // conversion per contributor; |error| <= ~1e-6, inside the 1e-4 tolerance);
 // expected depth, the dominant-weight pick and all decisions stay fp64.
 //
-// Top-K: each thread keeps the KMAX best (weight desc, source asc) entries in
-// registers by an unrolled insertion network (the reference's insertion select,
-// raster.cpp:238-249; proj order == source order). Selection only changes the
-// result when m > K, as in the reference (raster.cpp:442).
+// Top-K: each thread keeps its k_sel best (weight desc, source asc) entries sorted in
+// shared memory (slot-major) by insertion, with only the admission threshold in
+// registers (the reference's insertion select, raster.cpp:238-249; proj order ==
+// source order). Selection only changes the result when m > K, as in the reference
+// (raster.cpp:442).
 // Features: after compositing, each warp walks its 32 pixels; the owning lane's
 // (source, weight) slots are broadcast with __shfl_sync and the 32 lanes read the
 // selected surfel's feature row as one coalesced 128-512 B vector load and
