@@ -65,6 +65,26 @@ __device__ __forceinline__ int sort_class(int len) {
 // 0 for the longest lists (bit length 32) .. 32 for empty ones
 __device__ __forceinline__ int lpt_bucket(int len) { return __clz(len); }
 
+// Slot in a shared counter bucket for every active lane, one atomic per distinct bucket
+// of the warp (thousands of tiles land in the same few class / length buckets, so plain
+// per-thread shared atomics serialise on them). All lanes of the warp must call it.
+__device__ __forceinline__ int warp_bucket_slot(int* counters, int bucket, bool active) {
+  const unsigned am = __ballot_sync(0xffffffffu, active);
+  int slot = -1;
+  if (active) {
+    const int lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(am, bucket);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&counters[bucket], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    slot = base + __popc(peers & ((1u << lane) - 1u));
+  }
+  return slot;
+}
+
+constexpr int kScanLenTiles = 16384;  // tiles whose lpt bucket K3b keeps in shared memory
+
 // K3b: one CTA scans the tile totals: ranges, tile starts, RN-Total, non-empty tiles.
 __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ totals, int tiles, uint32_t cap,
                                                         int32_t* __restrict__ ranges, uint32_t* __restrict__ tile_start,
@@ -76,6 +96,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
   __shared__ uint32_t warp_ne[32];
   __shared__ int cls_n[kSortClasses];
   __shared__ int lpt_n[33];
+  __shared__ uint8_t lpt_s[kScanLenTiles];
   if (threadIdx.x < kSortClasses) cls_n[threadIdx.x] = 0;
   if (threadIdx.x < 33) lpt_n[threadIdx.x] = 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -112,6 +133,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
   uint32_t run = pre + x - local;
   for (int j = 0; j < per; ++j) {
     const int t = t0 + j;
+    int len = 0;
     if (t < tiles) {
       const uint32_t v = totals[t];
       tile_start[t] = run;
@@ -119,15 +141,23 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
       ranges[2 * t] = static_cast<int32_t>(b);
       ranges[2 * t + 1] = static_cast<int32_t>(e);
       run += v;
-      const int c = sort_class(static_cast<int>(e - b));
-      if (c >= 0) classes[c * tiles + atomicAdd(&cls_n[c], 1)] = t;
+      len = static_cast<int>(e - b);
+      if (t < kScanLenTiles) lpt_s[t] = static_cast<uint8_t>(lpt_bucket(len));
     }
+    const int c = t < tiles ? sort_class(len) : -1;
+    const int slot = warp_bucket_slot(cls_n, c < 0 ? 0 : c, c >= 0);
+    if (c >= 0) classes[c * tiles + slot] = t;
   }
+  // lpt bucket of tile t (kept in shared memory for the first kScanLenTiles tiles)
+  auto lpt_of = [&](int t) -> int {
+    return t < kScanLenTiles ? lpt_s[t] : lpt_bucket(ranges[2 * t + 1] - ranges[2 * t]);
+  };
   // Heaviest-first tile order for the blend's work items (longest-processing-time
   // scheduling by power-of-two bucket of the tile's list length): classes[5 tiles + i].
   for (int j = 0; j < per; ++j) {
     const int t = t0 + j;
-    if (t < tiles) atomicAdd(&lpt_n[lpt_bucket(ranges[2 * t + 1] - ranges[2 * t])], 1);
+    const int lb = t < tiles ? lpt_of(t) : 0;
+    warp_bucket_slot(lpt_n, lb, t < tiles);
   }
   __syncthreads();
   if (tid == 0) {
@@ -141,8 +171,9 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
   __syncthreads();
   for (int j = 0; j < per; ++j) {
     const int t = t0 + j;
-    if (t < tiles)
-      classes[(kSortClasses + 1) * tiles + atomicAdd(&lpt_n[lpt_bucket(ranges[2 * t + 1] - ranges[2 * t])], 1)] = t;
+    const int lb = t < tiles ? lpt_of(t) : 0;
+    const int slot = warp_bucket_slot(lpt_n, lb, t < tiles);
+    if (t < tiles) classes[(kSortClasses + 1) * tiles + slot] = t;
   }
   if (tid < kSortClasses) classes[kSortClasses * tiles + tid] = cls_n[tid];
   if (tid == 0) {
