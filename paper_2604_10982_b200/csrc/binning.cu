@@ -276,6 +276,14 @@ constexpr int kEmitWarps = 8;
 #ifndef PSM_EMIT_MINB
 #define PSM_EMIT_MINB 4
 #endif
+// Surfels per warp: 32 (one per lane), or fewer for small scenes, whose few warps would
+// otherwise each carry 32 surfels: a warp of 32 full-image footprints (C1's ground near
+// the camera) then holds the launch alone for tens of microseconds of atomic round trips
+// (C1 emit: 32 surfels per warp 84 us, 8: 29 us, 4: 19.5 us, 2: 16.4 us).
+#ifndef PSM_EMIT_SMALL_SPW
+#define PSM_EMIT_SMALL_SPW 2
+#endif
+template <int SPW>
 __global__ void __launch_bounds__(32 * kEmitWarps, PSM_EMIT_MINB) emit_kernel(const int32_t* __restrict__ valid, int64_t n,
                                                    const SurfRec* __restrict__ recs, const BinRec* __restrict__ bins,
                                                    DevRaster rs, int img_h, uint32_t* __restrict__ cursor,
@@ -286,12 +294,13 @@ __global__ void __launch_bounds__(32 * kEmitWarps, PSM_EMIT_MINB) emit_kernel(co
                                                    int img_w) {
   __shared__ EmitItem items[kEmitWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t i = (static_cast<int64_t>(blockIdx.x) * kEmitWarps + warp) * 32 + lane;
+  const int64_t wbase = (static_cast<int64_t>(blockIdx.x) * kEmitWarps + warp) * SPW;
+  const int64_t i = wbase + lane;
   const bool ellipse = rs.binning == PSM_BIN_ELLIPSE;
   // warp-block masks need the support cutoff (a pixel only uses candidates passing it)
   const bool masks_on = rs.support_cutoff != 0;
   int rows = 0;
-  if (i < n && valid[i]) {
+  if (lane < SPW && i < n && valid[i]) {
     const BinRec b = bins[i];
     if (b.tx0 <= b.tx1 && b.ty0 <= b.ty1) {
       EmitItem& it = items[warp][lane];
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(32 * kEmitWarps, PSM_EMIT_MINB) emit_kernel(co
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   __syncwarp();
 
-  // a pair's sub-bucket is its surfel's lane (K1 counted it there: source & (kSplit - 1))
+  // a pair's sub-bucket is source & (kSplit - 1), where K1 counted it
   const int64_t n_tiles = static_cast<int64_t>(rs.tiles_x) * rs.tiles_y;
   // tiles are claimed in batches of kBatch so several returning atomics are in flight at once
   constexpr int kBatch = 8;
@@ -332,7 +341,10 @@ __global__ void __launch_bounds__(32 * kEmitWarps, PSM_EMIT_MINB) emit_kernel(co
     uint32_t o[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; ++u)
-      if (u < np) o[u] = atomicAdd(cursor + ((pend[u] >> 19) & 31u) * n_tiles + (pend[u] & 0x7ffffu), 1u);
+      if (u < np) {
+        const uint32_t split = (static_cast<uint32_t>(wbase) + ((pend[u] >> 19) & 31u)) & 31u;  // source & 31
+        o[u] = atomicAdd(cursor + split * n_tiles + (pend[u] & 0x7ffffu), 1u);
+      }
 #pragma unroll
     for (int u = 0; u < kBatch; ++u)
       if (u < np) {
@@ -730,10 +742,14 @@ void launch_emit(const int32_t* valid, int64_t n, const SurfRec* recs, const Bin
                  int img_h, uint32_t* cursor, const uint32_t* tile_start, uint32_t cap, uint64_t* tile_keys,
                  const uint64_t* depth_bits, const unsigned long long* depth_minmax, int src_bits, int img_w,
                  cudaStream_t st) {
-  if (n > 0)
-    emit_kernel<<<grid_for(n, 32 * kEmitWarps), 32 * kEmitWarps, 0, st>>>(valid, n, recs, bins, rs, img_h, cursor,
-                                                                          tile_start, cap, tile_keys, depth_bits,
-                                                                          depth_minmax, src_bits, img_w);
+  if (n <= 0) return;
+  // fewer than ~4 CTAs of 32-surfel warps per SM: PSM_EMIT_SMALL_SPW surfels per warp
+  if (n < 148LL * 4 * kEmitWarps * 32)
+    emit_kernel<PSM_EMIT_SMALL_SPW><<<grid_for(n, PSM_EMIT_SMALL_SPW * kEmitWarps), 32 * kEmitWarps, 0, st>>>(
+        valid, n, recs, bins, rs, img_h, cursor, tile_start, cap, tile_keys, depth_bits, depth_minmax, src_bits, img_w);
+  else
+    emit_kernel<32><<<grid_for(n, 32 * kEmitWarps), 32 * kEmitWarps, 0, st>>>(
+        valid, n, recs, bins, rs, img_h, cursor, tile_start, cap, tile_keys, depth_bits, depth_minmax, src_bits, img_w);
 }
 
 template <int NT, int CLS>
