@@ -273,6 +273,11 @@ struct EmitItem {
 };
 constexpr int kEmitWarps = 8;
 
+// returning atomics in flight per thread (C3 emit, measured: 8 at 4 CTAs/SM 0.098 ms;
+// 8 / 12 / 16 at 3 CTAs 0.112 / 0.113 / 0.131; 16 at 4 CTAs spills, 0.115)
+#ifndef PSM_EMIT_BATCH
+#define PSM_EMIT_BATCH 8
+#endif
 #ifndef PSM_EMIT_MINB
 #define PSM_EMIT_MINB 4
 #endif
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(32 * kEmitWarps, PSM_EMIT_MINB) emit_kernel(co
   // a pair's sub-bucket is source & (kSplit - 1), where K1 counted it
   const int64_t n_tiles = static_cast<int64_t>(rs.tiles_x) * rs.tiles_y;
   // tiles are claimed in batches of kBatch so several returning atomics are in flight at once
-  constexpr int kBatch = 8;
+  constexpr int kBatch = PSM_EMIT_BATCH;
   uint32_t pend[kBatch];  // tile index | owner lane << 19 | block mask << 24
   int np = 0;
   auto flush = [&]() {
