@@ -363,6 +363,94 @@ struct Outputs {
   int32_t *ins_argmax, *blend_count;
 };
 
+
+// ---------------------------------------------------------------- workload (synthetic.cpp)
+// make_street_scene (synthetic.cpp:236-312) with Camera::look_at (core_types.cpp:40-60),
+// quat_from_axes (synthetic.cpp:21-27), quat_from_rotation (math_util.cpp:73-92) and Rng
+// (math_util.hpp:27-63), plus the scale_mult density knob of SURVEY.md §8d (s1 *= k right
+// after its draw). Operand draws follow the order GCC gives the reference's expressions
+// (right to left; pinned against oracle/_ref by tests/test_ref_pin.py).
+struct SplitMix {
+  uint64_t state;
+  uint64_t next() {
+    uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  }
+  double u01() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  double uni(double lo, double hi) { return lo + (hi - lo) * u01(); }
+  double gauss() {
+    double a = u01();
+    const double b = u01();
+    if (a < 1e-300) a = 1e-300;
+    return std::sqrt(-2.0 * std::log(a)) * std::cos(2.0 * M_PI * b);
+  }
+};
+inline V3 v3(double x, double y, double z) { return V3{{x, y, z}}; }
+inline V3 vadd(const V3& a, const V3& b) { return v3(a.v[0] + b.v[0], a.v[1] + b.v[1], a.v[2] + b.v[2]); }
+inline V3 vmul(double s, const V3& a) { return v3(s * a.v[0], s * a.v[1], s * a.v[2]); }
+inline V3 vcross(const V3& a, const V3& b) {
+  return v3(a.v[1] * b.v[2] - a.v[2] * b.v[1], a.v[2] * b.v[0] - a.v[0] * b.v[2], a.v[0] * b.v[1] - a.v[1] * b.v[0]);
+}
+inline V3 vnormalized(const V3& a) {  // MatrixBase::normalized: a / sqrt(squaredNorm) when > 0
+  const double z = dot3(a, a);
+  return z > 0 ? v3(a.v[0] / std::sqrt(z), a.v[1] / std::sqrt(z), a.v[2] / std::sqrt(z)) : a;
+}
+// quat_from_rotation (math_util.cpp:73-92); M3 column-major like Eigen.
+void quat_of(const M3& r, double q[4]) {
+  const double tr = sum3(r.at(0, 0), r.at(1, 1), r.at(2, 2));
+  if (tr > 0) {
+    const double s = std::sqrt(tr + 1.0) * 2;
+    q[0] = 0.25 * s; q[1] = (r.at(2, 1) - r.at(1, 2)) / s; q[2] = (r.at(0, 2) - r.at(2, 0)) / s;
+    q[3] = (r.at(1, 0) - r.at(0, 1)) / s;
+  } else if (r.at(0, 0) > r.at(1, 1) && r.at(0, 0) > r.at(2, 2)) {
+    const double s = std::sqrt(1.0 + r.at(0, 0) - r.at(1, 1) - r.at(2, 2)) * 2;
+    q[0] = (r.at(2, 1) - r.at(1, 2)) / s; q[1] = 0.25 * s; q[2] = (r.at(0, 1) + r.at(1, 0)) / s;
+    q[3] = (r.at(0, 2) + r.at(2, 0)) / s;
+  } else if (r.at(1, 1) > r.at(2, 2)) {
+    const double s = std::sqrt(1.0 + r.at(1, 1) - r.at(0, 0) - r.at(2, 2)) * 2;
+    q[0] = (r.at(0, 2) - r.at(2, 0)) / s; q[1] = (r.at(0, 1) + r.at(1, 0)) / s; q[2] = 0.25 * s;
+    q[3] = (r.at(1, 2) + r.at(2, 1)) / s;
+  } else {
+    const double s = std::sqrt(1.0 + r.at(2, 2) - r.at(0, 0) - r.at(1, 1)) * 2;
+    q[0] = (r.at(1, 0) - r.at(0, 1)) / s; q[1] = (r.at(0, 2) + r.at(2, 0)) / s; q[2] = (r.at(1, 2) + r.at(2, 1)) / s;
+    q[3] = 0.25 * s;
+  }
+  if (q[0] < 0) for (int i = 0; i < 4; ++i) q[i] = -q[i];
+  const double n = std::sqrt((q[0] * q[0] + q[2] * q[2]) + (q[1] * q[1] + q[3] * q[3]));  // Vector4d::norm
+  for (int i = 0; i < 4; ++i) q[i] = q[i] / n;
+}
+void quat_axes(const V3& tu, const V3& tv, double q[4]) {  // synthetic.cpp:21-27
+  M3 r;
+  const V3 c0 = vnormalized(tu), c2 = vnormalized(vcross(tu, tv)), c1 = vcross(c2, c0);
+  for (int i = 0; i < 3; ++i) { r.at(i, 0) = c0.v[i]; r.at(i, 1) = c1.v[i]; r.at(i, 2) = c2.v[i]; }
+  quat_of(r, q);
+}
+// Camera::look_at (core_types.cpp:40-60) -> psm_camera (r_cw column-major).
+bool look_at(const V3& eye, const V3& target, const V3& up, double fx, double fy, int w, int h, double nc,
+             double fc, psm_camera* out) {
+  V3 fwd = v3(target.v[0] - eye.v[0], target.v[1] - eye.v[1], target.v[2] - eye.v[2]);
+  if (norm3(fwd) < 1e-12) return false;
+  fwd = vnormalized(fwd);
+  V3 right = vcross(fwd, up);
+  if (norm3(right) < 1e-9) {
+    right = vcross(fwd, v3(1, 0, 0));
+    if (norm3(right) < 1e-9) right = vcross(fwd, v3(0, 1, 0));
+  }
+  right = vnormalized(right);
+  const V3 down = vcross(fwd, right);
+  M3 rcw;  // r_wc = [right down fwd]; r_cw = r_wc^T
+  for (int j = 0; j < 3; ++j) { rcw.at(0, j) = right.v[j]; rcw.at(1, j) = down.v[j]; rcw.at(2, j) = fwd.v[j]; }
+  M3 neg;
+  for (int i = 0; i < 9; ++i) neg.m[i] = -rcw.m[i];
+  const V3 t = matvec(neg, eye);  // -r_cw * eye
+  std::memcpy(out->r_cw, rcw.m, sizeof out->r_cw);
+  for (int i = 0; i < 3; ++i) out->t_cw[i] = t.v[i];
+  out->fx = fx; out->fy = fy; out->cx = 0.5 * w; out->cy = 0.5 * h;
+  out->width = w; out->height = h; out->near_clip = nc; out->far_clip = fc;
+  return true;
+}
 }  // namespace
 
 extern "C" {
@@ -527,6 +615,68 @@ typedef struct oracle_cache {
   double* alpha;     // [cap]
   int64_t cap;
 } oracle_cache;
+
+
+// make_street_scene on the oracle (see the workload section). Two-phase like
+// psm_make_street_scene: NULL surfels13 returns n (and the camera) only.
+int oracle_make_street_scene(const psm_street_spec* spec, int64_t* n_out, double* surfels13, double* f_sem,
+                             double* labels, double* f_ins, psm_camera* cam) {
+  struct Group { V3 o, e1, e2; int inst; double share; };
+  std::vector<Group> gs = {{v3(-4, 1.5, 1.5), v3(8, 0, 0), v3(0, 0, 38), 0, 0.10},
+                           {v3(-4.0, 1.5, 1.5), v3(0.9, -4.0, 0), v3(0, 0, 38), 1, 0.06},
+                           {v3(4.0, 1.5, 1.5), v3(-0.9, -4.0, 0), v3(0, 0, 38), 2, 0.06}};
+  const int ninst = spec->n_instances, layers = 18;
+  const int bands = std::max(1, (ninst - 3) / layers + 1);
+  for (int l = 0; l < layers; ++l)
+    for (int b = 0; b < bands; ++b) {
+      const double bw = 7.2 / bands;
+      gs.push_back({v3(-3.6 + b * bw, -2.6, 3.2 + 2.0 * l), v3(bw, 0, 0), v3(0, 5.2, 0),
+                    3 + (b % std::max(1, ninst - 3)), 0.78 / (layers * bands)});
+    }
+  std::vector<int> counts;
+  int64_t n = 0;
+  for (const Group& g : gs) {
+    counts.push_back(static_cast<int>(std::round(g.share * spec->n_surfels)));
+    n += counts.back();
+  }
+  *n_out = n;
+  if (cam && !look_at(v3(0, 0, 0), v3(0, 0, 20), v3(0, -1, 0), 0.8 * spec->image_w, 0.8 * spec->image_w,
+                      spec->image_w, spec->image_h, 0.1, 200.0, cam))
+    return PSM_EINVAL;
+  if (!surfels13) return PSM_OK;
+  SplitMix rng{spec->seed};
+  const double k = spec->scale_mult > 0 ? spec->scale_mult : 1.0;
+  int64_t at = 0;
+  for (size_t gi = 0; gi < gs.size(); ++gi) {
+    const Group& g = gs[gi];
+    const V3 u1 = vnormalized(g.e1), u2 = vnormalized(g.e2), nrm = vnormalized(vcross(u1, u2));
+    for (int i = 0; i < counts[gi]; ++i, ++at) {
+      double* s = surfels13 + 13 * at;
+      const double jit = rng.uni(-0.03, 0.03), b2 = rng.u01(), b1 = rng.u01();  // right-to-left operands
+      const V3 c = vadd(vadd(vadd(g.o, vmul(b1, g.e1)), vmul(b2, g.e2)), vmul(jit, nrm));
+      for (int d = 0; d < 3; ++d) s[d] = c.v[d];
+      const double phi = rng.uni(0, M_PI);
+      quat_axes(vadd(vmul(std::cos(phi), u1), vmul(std::sin(phi), u2)),
+                vadd(vmul(-std::sin(phi), u1), vmul(std::cos(phi), u2)), s + 3);
+      const double s1 = rng.uni(0.45, 1.1) * k;
+      const double aspect = rng.uni(spec->min_aspect, 2.0 * spec->min_aspect);
+      s[7] = s1; s[8] = s1 / aspect;
+      s[9] = rng.uni(0.30, 0.70);
+      for (int d = 2; d >= 0; --d) s[10 + d] = rng.uni(0.2, 0.9);  // Vec3(u, u, u) constructor args
+      for (int c2 = 0; c2 < spec->c_sem; ++c2) {
+        const double v = rng.gauss();
+        if (f_sem) f_sem[at * spec->c_sem + c2] = v;
+      }
+      for (int c2 = 0; c2 < 8; ++c2) {
+        const double v = 0.3 * rng.gauss();
+        if (f_ins) f_ins[at * 8 + c2] = v;
+      }
+      if (labels)
+        for (int q = 0; q < ninst; ++q) labels[at * ninst + q] = q == g.inst ? 0.92 : 0.08 / (ninst - 1);
+    }
+  }
+  return PSM_OK;
+}
 
 // Backward state (pipeline.cpp:347-460): upstream plane gradients in, per-surfel sums out.
 struct BackwardAcc {

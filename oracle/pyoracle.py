@@ -121,6 +121,27 @@ def bin_surfels(surfels13, cam, cfg, binning: int, chi2: Optional[float] = None)
             "rn_per_tile": float(cnt.rn_per_tile), "per_surfel": per[:n].copy(), "n_proj": int(cnt.n_proj)}
 
 
+def make_street_scene(spec, with_labels: bool = False, with_f_ins: bool = False):
+    """make_street_scene (synthetic.cpp:236-312, + scale_mult) on the oracle: (surfels13 (N,13),
+    f_sem (N,C), labels (N,n_instances) or None, psm_camera[, f_ins (N,8)]). Loads no product code."""
+    lib = load()
+    fn = lib.oracle_make_street_scene
+    fn.restype = C.c_int
+    fn.argtypes = [C.POINTER(A.psm_street_spec), C.POINTER(C.c_int64), C.c_void_p, C.c_void_p, C.c_void_p,
+                   C.c_void_p, C.POINTER(A.psm_camera)]
+    cs = spec.to_c()
+    n = C.c_int64()
+    cam = A.psm_camera()
+    if fn(C.byref(cs), C.byref(n), None, None, None, None, C.byref(cam)) != 0:
+        raise ValueError("make_street_scene failed")
+    s = np.empty((n.value, 13))
+    f = np.empty((n.value, spec.c_sem))
+    lab = np.empty((n.value, spec.n_instances)) if with_labels else None
+    fi = np.empty((n.value, 8)) if with_f_ins else None
+    fn(C.byref(cs), C.byref(n), _p(s), _p(f), _p(lab), _p(fi), C.byref(cam))
+    return (s, f, lab, cam, fi) if with_f_ins else (s, f, lab, cam)
+
+
 def psm_exp(x) -> np.ndarray:
     xs = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
     out = np.empty_like(xs)

@@ -1,0 +1,202 @@
+"""ctypes wrapper of oracle/_ref/libpsimap_ref.so: the REFERENCE'S OWN render path
+(/root/reference/proj/src/{raster,math_util,core_types,synthetic}.cpp, compiled unchanged
+by oracle/ref/Makefile against the minimal Eigen stand-in oracle/eigen_min).
+TEST INFRASTRUCTURE ONLY: imported by tests/ and by bench.py's reference arm, never by
+the product package.
+
+`available()` is False where the library was not built (it needs /root/reference at
+build time; the built .so travels to the GPU box with the repo snapshot).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "_ref", "libpsimap_ref.so")
+REF_SRC = "/root/reference/proj/src/raster.cpp"
+_lib = None
+
+
+def _abi():
+    # struct layouts of include/psm.h (plain ctypes; importing _abi does not load libpsm.so)
+    from paper_2604_10982_b200 import _abi as A
+    return A
+
+
+class ref_projected(C.Structure):
+    _fields_ = [("status", C.c_int32), ("center", C.c_double * 2), ("sigma", C.c_double * 4),
+                ("sort_depth", C.c_double), ("h", C.c_double * 9), ("h_inv", C.c_double * 9),
+                ("finv", C.c_double * 4), ("normal_vis", C.c_double * 3)]
+
+
+def build() -> bool:
+    """Builds oracle/_ref when the reference tree is present (this container only)."""
+    if not os.path.exists(REF_SRC):
+        return os.path.exists(LIB)
+    subprocess.run(["make", "-s", "-C", os.path.join(HERE, "ref")], check=True)
+    return True
+
+
+def available() -> bool:
+    return os.path.exists(LIB) or os.path.exists(REF_SRC)
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB):
+        build()
+    A = _abi()
+    lib = C.CDLL(LIB)
+    vp, P = C.c_void_p, C.POINTER
+    sig = {
+        "ref_make_street_scene": (C.c_int, [P(A.psm_street_spec), P(C.c_int64), vp, vp, vp, vp, P(A.psm_camera)]),
+        "ref_camera_look_at": (C.c_int, [vp, vp, vp, C.c_double, C.c_double, C.c_int32, C.c_int32, C.c_double,
+                                         C.c_double, P(A.psm_camera)]),
+        "ref_scene_create": (vp, [vp, C.c_int64, vp, C.c_int32, vp, C.c_int32]),
+        "ref_scene_free": (None, [vp]),
+        "ref_render_into": (C.c_int, [vp, P(A.psm_camera), P(A.psm_raster_config), P(C.c_uint64)]),
+        "ref_targets_copy": (None, [vp] * 9),
+        "ref_bin": (C.c_int, [vp, P(A.psm_camera), P(A.psm_raster_config), C.c_int32, C.c_double, vp, vp,
+                              C.c_int64, P(A.psm_counters)]),
+        "ref_project_surfel": (C.c_int, [vp, P(A.psm_camera), P(A.psm_raster_config), P(ref_projected)]),
+        "ref_evaluate_alpha": (C.c_double, [vp, P(A.psm_camera), C.c_double, C.c_double, P(A.psm_raster_config),
+                                            P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_int32)]),
+        "ref_topk_select": (None, [vp, vp, C.c_int32, C.c_int32, vp]),
+        "ref_bench_render": (C.c_int, [vp, P(A.psm_camera), C.c_int32, P(A.psm_raster_config), vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype, fn.argtypes = res, args
+    _lib = lib
+    return lib
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None or a.size == 0 else a.ctypes.data_as(C.c_void_p)
+
+
+def make_street_scene(n_surfels=12000, seed=7, min_aspect=5.0, image_w=256, image_h=192, c_sem=32,
+                      n_instances=256, labels=True):
+    """make_street_scene (synthetic.cpp:236-312) exactly as the reference generates it:
+    (surfels13 (N,13), f_sem (N,C), labels (N,n_instances) or None, f_ins (N,8), psm_camera)."""
+    A = _abi()
+    lib = load()
+    spec = A.psm_street_spec(n_surfels, seed, min_aspect, image_w, image_h, c_sem, n_instances, 1.0)
+    n = C.c_int64()
+    cam = A.psm_camera()
+    if lib.ref_make_street_scene(C.byref(spec), C.byref(n), None, None, None, None, C.byref(cam)) != 0:
+        raise ValueError("make_street_scene failed")
+    s = np.empty((n.value, 13))
+    f = np.empty((n.value, c_sem))
+    lab = np.empty((n.value, n_instances)) if labels else None
+    fi = np.empty((n.value, 8))
+    lib.ref_make_street_scene(C.byref(spec), C.byref(n), _p(s), _p(f), _p(lab), _p(fi), C.byref(cam))
+    return s, f, lab, fi, cam
+
+
+class RefScene:
+    """A psimap::SceneMap (+ labels MatX) held by the reference library, rendered with render_into."""
+
+    def __init__(self, surfels13, f_sem=None, labels=None):
+        self.lib = load()
+        self.surfels = np.ascontiguousarray(np.asarray(surfels13, dtype=np.float64).reshape(-1, 13))
+        n = self.surfels.shape[0]
+        f = np.zeros((n, 0)) if f_sem is None else np.ascontiguousarray(np.asarray(f_sem, dtype=np.float64))
+        self.c_sem = f.shape[1] if n else 0
+        lab = None if labels is None else np.ascontiguousarray(np.asarray(labels, dtype=np.float64))
+        self.n_q = 0 if lab is None else lab.shape[1]
+        self.h = self.lib.ref_scene_create(_p(self.surfels), n, _p(f), self.c_sem, _p(lab), self.n_q)
+
+    def close(self):
+        if self.h:
+            self.lib.ref_scene_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def render_into(self, cam_c, cfg_c) -> int:
+        """One render_into (raster.cpp:273-511); returns blended_total. Raises on a degenerate quaternion."""
+        bt = C.c_uint64()
+        st = self.lib.ref_render_into(self.h, C.byref(cam_c), C.byref(cfg_c), C.byref(bt))
+        if st != 0:
+            raise ValueError("degenerate quaternion")
+        return int(bt.value)
+
+    def render(self, cam, cfg) -> dict:
+        """render (raster.cpp:266-271): fp64 planes (H, W, C) and blended_total."""
+        bt = self.render_into(cam.to_c(), cfg.to_c())
+        w, h = cam.width, cam.height
+        out = {"color": np.zeros((h, w, 3)), "depth": np.zeros((h, w, 2)), "normal": np.zeros((h, w, 3)),
+               "sem_feat": np.zeros((h, w, self.c_sem)), "ins_dist": np.zeros((h, w, self.n_q)),
+               "ins_argmax": np.zeros((h, w, 1), np.int32), "alpha_acc": np.zeros((h, w, 1)),
+               "blend_count": np.zeros((h, w, 1), np.int32)}
+        self.lib.ref_targets_copy(self.h, *[_p(out[k]) for k in ("color", "depth", "normal", "sem_feat", "ins_dist",
+                                                                  "ins_argmax", "alpha_acc", "blend_count")])
+        out["blended_total"] = bt
+        return out
+
+    def bin(self, cam, cfg, binning: int, chi2: Optional[float] = None) -> dict:
+        """project_surfel + bin_circle / bin_aabb: per-tile source-id lists and TileGrid counters."""
+        A = _abi()
+        c, k = cam.to_c(), cfg.to_c()
+        chi = cfg.chi2 if chi2 is None else chi2
+        tiles = ((cam.width + cfg.tile_size - 1) // cfg.tile_size) * ((cam.height + cfg.tile_size - 1) // cfg.tile_size)
+        counts = np.zeros(tiles, np.int32)
+        cnt = A.psm_counters()
+        if self.lib.ref_bin(self.h, C.byref(c), C.byref(k), binning, chi, _p(counts), None, 0, C.byref(cnt)) != 0:
+            raise ValueError("degenerate quaternion")
+        total = int(counts.sum())
+        lists = np.zeros(max(total, 1), np.int32)
+        self.lib.ref_bin(self.h, C.byref(c), C.byref(k), binning, chi, None, _p(lists), total, None)
+        offs = np.concatenate([[0], np.cumsum(counts)])
+        return {"tiles": [lists[offs[t]:offs[t + 1]].copy() for t in range(tiles)], "counts": counts,
+                "lists": lists[:total], "rn_total": int(cnt.rn_total), "rn_per_tile": float(cnt.rn_per_tile),
+                "n_proj": int(cnt.n_proj)}
+
+    def bench_render(self, cam, reps: int, cfg) -> list:
+        """bench_render (raster.cpp:513-573): rows (time_ms, fps, rn_total, rn_per_tile, blended, per_pixel)."""
+        rows = np.zeros((4, 6))
+        if self.lib.ref_bench_render(self.h, C.byref(cam.to_c()), reps, C.byref(cfg.to_c()), _p(rows)) != 0:
+            raise ValueError("degenerate quaternion")
+        return rows
+
+
+def project_surfel(s13, cam, cfg) -> Optional[dict]:
+    s = np.ascontiguousarray(np.asarray(s13, dtype=np.float64).reshape(13))
+    out = ref_projected()
+    st = load().ref_project_surfel(_p(s), C.byref(cam.to_c()), C.byref(cfg.to_c()), C.byref(out))
+    if st < 0:
+        raise ValueError("degenerate quaternion")
+    if st == 0:
+        return None
+    return {"center": np.array(list(out.center)), "sigma": np.array(list(out.sigma)).reshape(2, 2).T,
+            "sort_depth": out.sort_depth, "h": np.array(list(out.h)).reshape(3, 3).T,
+            "h_inv": np.array(list(out.h_inv)).reshape(3, 3).T,
+            "footprint_inv": np.array(list(out.finv)).reshape(2, 2).T, "normal_vis": np.array(list(out.normal_vis))}
+
+
+def evaluate_alpha(s13, cam, px, py, cfg) -> dict:
+    s = np.ascontiguousarray(np.asarray(s13, dtype=np.float64).reshape(13))
+    u, v, w2, inside = C.c_double(), C.c_double(), C.c_double(), C.c_int32()
+    a = load().ref_evaluate_alpha(_p(s), C.byref(cam.to_c()), px, py, C.byref(cfg.to_c()), C.byref(u), C.byref(v),
+                                  C.byref(w2), C.byref(inside))
+    return {"alpha": a, "u": u.value, "v": v.value, "w2": w2.value, "inside": bool(inside.value)}
+
+
+def topk_select(weights, proj, k: int) -> np.ndarray:
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+    p = np.ascontiguousarray(np.asarray(proj, dtype=np.int32))
+    sel = np.zeros(len(w), dtype=np.int8)
+    load().ref_topk_select(_p(w), _p(p), len(w), k, _p(sel))
+    return sel.astype(bool)

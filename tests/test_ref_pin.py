@@ -1,0 +1,201 @@
+"""Pins the CPU oracle (oracle/oracle.cpp) and the host workload generator to the REFERENCE'S
+OWN CODE: proj/src/{raster,math_util,core_types,synthetic}.cpp compiled unchanged into
+oracle/_ref (oracle/ref/Makefile, against the minimal Eigen stand-in oracle/eigen_min).
+
+Bit-exact, every fp64 / int32 plane of render_into (raster.cpp:273-511), the tile lists of
+bin_circle / bin_aabb (raster.cpp:51-90,144-152), the bench_render counters
+(raster.cpp:513-573), the stage functions (project_surfel, evaluate_alpha, topk_select), the
+street-scene generator (synthetic.cpp:236-312) and Camera::look_at (core_types.cpp:40-60).
+Non-identity camera poses (the C5 trajectory, an arbitrary Camera::make pose) exercise the
+camera transform products (raster.cpp:96-101, core_types.hpp:51-52) bit for bit.
+
+The oracle's parity build uses psm_exp (the GPU's exp); the libm build uses glibc exp like
+the reference. Both must match the reference exactly: psm_exp restates glibc's FMA exp.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from oracle import pyref as R
+from paper_2604_10982_b200 import (Binning, Blending, Camera, RasterConfig, SceneMap, StreetSpec, density_scale,
+                                   make_street_scene, trajectory_cameras)
+from tests.helpers import Rng
+
+pytestmark = pytest.mark.skipif(not R.available(), reason="oracle/_ref not built (needs /root/reference)")
+
+PLANES = ("color", "depth", "normal", "sem_feat", "ins_dist", "ins_argmax", "alpha_acc", "blend_count")
+
+
+def assert_oracle_is_reference(rs: R.RefScene, scene, labels, cam, cfg, libm_too=True):
+    r = rs.render(cam, cfg)
+    for libm in ((False, True) if libm_too else (False,)):
+        o = O.render(scene, labels, cam, cfg, libm=libm)
+        for k in PLANES:
+            assert r[k].shape == o[k].shape, k
+            assert np.array_equal(r[k], o[k]), (k, "libm" if libm else "psm_exp",
+                                                 int(np.count_nonzero(r[k] != o[k])))
+        assert r["blended_total"] == o["counters"]["blended_total"]
+    return r
+
+
+@pytest.fixture(scope="module")
+def c0():
+    """C0: the reference-standard street scene (12k surfels, 256x192, C_sem 32, 256 labels, seed 7)."""
+    s, f, lab, fi, camc = R.make_street_scene()
+    return s, f, lab, fi, Camera.from_c(camc), R.RefScene(s, f, lab)
+
+
+def test_street_scene_generator_is_the_reference(c0):
+    s, f, lab, fi, cam, _ = c0
+    sc, lab2, cam2 = make_street_scene(StreetSpec())
+    assert np.array_equal(sc.surfels, s) and np.array_equal(sc.f_sem, f) and np.array_equal(lab2, lab)
+    assert bytes(cam2.to_c()) == bytes(cam.to_c())
+    from paper_2604_10982_b200 import street_f_ins
+    assert np.array_equal(street_f_ins(StreetSpec()), fi)
+
+
+def test_street_scene_generator_c3_shape_and_scale_mult():
+    """C3-shaped spec (1280x720, C_sem 64). scale_mult multiplies s1 right after it is
+    drawn: every other draw, and s1 itself up to that product, is the reference's."""
+    kw = dict(n_surfels=20000, image_w=1280, image_h=720, c_sem=64, n_instances=32)
+    s, f, lab, fi, camc = R.make_street_scene(**kw)
+    sc, lab2, cam2 = make_street_scene(StreetSpec(**kw))
+    assert np.array_equal(sc.surfels, s) and np.array_equal(sc.f_sem, f) and np.array_equal(lab2, lab)
+    assert bytes(cam2.to_c()) == bytes(camc)
+    k = density_scale(20000, 1280, 720)
+    sk, _, _ = make_street_scene(StreetSpec(scale_mult=k, **kw), with_labels=False)
+    other = [c for c in range(13) if c not in (7, 8)]
+    assert np.array_equal(sk.surfels[:, other], s[:, other]) and np.array_equal(sk.f_sem, f)
+    assert np.array_equal(sk.surfels[:, 7], s[:, 7] * k)
+    np.testing.assert_allclose(sk.surfels[:, 8], s[:, 8] * k, rtol=1e-14)
+
+
+def test_oracle_generator_is_the_reference():
+    """The oracle's own generator (used by bench.py's reference arm) equals the reference's."""
+    kw = dict(n_surfels=5000, image_w=320, image_h=180, c_sem=16, n_instances=8)
+    s, f, lab, _, camc = R.make_street_scene(**kw)
+    so, fo, labo, camo = O.make_street_scene(StreetSpec(**kw), with_labels=True)
+    assert np.array_equal(so, s) and np.array_equal(fo, f) and np.array_equal(labo, lab)
+    assert bytes(camo) == bytes(camc)
+
+
+def test_look_at_is_the_reference():
+    import ctypes as C
+    from paper_2604_10982_b200 import _abi as A
+    for i in (0, 1, 37, 64, 128, 200, 255):
+        a = 2.0 * math.pi * i / 256
+        eye = (0.8 * math.sin(a), 0.2 * math.sin(2.0 * a), 0.05 * i)
+        th = 0.15 * math.sin(a)
+        tgt = (eye[0] + 20.0 * math.sin(th), eye[1], eye[2] + 20.0 * math.cos(th))
+        ours = trajectory_cameras(256, 1920, 1080, first=i, count=1)[0]
+        rc = A.psm_camera()
+        arr = lambda v: (C.c_double * 3)(*v)
+        assert R.load().ref_camera_look_at(arr(eye), arr(tgt), arr((0.0, -1.0, 0.0)), 0.8 * 1920, 0.8 * 1920, 1920,
+                                           1080, 0.1, 200.0, C.byref(rc)) == 0
+        assert bytes(ours.to_c()) == bytes(rc), i
+
+
+@pytest.mark.parametrize("binning", [Binning.Circle, Binning.Aabb])
+@pytest.mark.parametrize("blending,k", [(Blending.Full, 16), (Blending.TopK, 16), (Blending.TopK, 8)])
+def test_oracle_is_reference_c0(c0, binning, blending, k):
+    s, f, lab, _, cam, rs = c0
+    assert_oracle_is_reference(rs, SceneMap(s, f), lab, cam, RasterConfig(binning=binning, blending=blending, top_k=k))
+
+
+def test_oracle_is_reference_config_variants(c0):
+    s, f, lab, _, cam, rs = c0
+    sc = SceneMap(s, f)
+    for cfg in (RasterConfig(support_cutoff=False), RasterConfig(render_depth_normal=False, blending=Blending.TopK),
+                RasterConfig(background=(0.2, 0.4, 0.6), t_min=1e-2, alpha_min=0.05, chi2=4.0),
+                RasterConfig(blending=Blending.TopK, top_k=1), RasterConfig(blending=Blending.TopK, top_k=0),
+                RasterConfig(tile_size=8), RasterConfig(tile_size=32, blending=Blending.TopK, top_k=5)):
+        assert_oracle_is_reference(rs, sc, lab, cam, cfg, libm_too=False)
+
+
+def test_bin_lists_are_reference(c0):
+    s, f, lab, _, cam, rs = c0
+    for cams in ([cam], trajectory_cameras(256, 256, 192, first=3, count=1)):
+        for binning in (Binning.Circle, Binning.Aabb):
+            cfg = RasterConfig(binning=binning)
+            r = rs.bin(cams[0], cfg, binning)
+            o = O.bin_surfels(s, cams[0], cfg, binning)
+            assert r["rn_total"] == o["rn_total"] and r["n_proj"] == o["n_proj"]
+            assert r["rn_per_tile"] == o["rn_per_tile"]
+            assert all(np.array_equal(a, b) for a, b in zip(r["tiles"], o["tiles"]))
+
+
+def test_bench_render_counters_are_reference(c0):
+    """bench_render rows (raster.cpp:513-573): rn_total, rn_per_tile, blended_total identical."""
+    s, f, lab, _, cam, rs = c0
+    rows = rs.bench_render(cam, 1, RasterConfig(top_k=16))
+    for i, (binning, blending) in enumerate([(Binning.Circle, Blending.Full), (Binning.Aabb, Blending.Full),
+                                             (Binning.Circle, Blending.TopK), (Binning.Aabb, Blending.TopK)]):
+        o = O.render(SceneMap(s, f), lab, cam, RasterConfig(binning=binning, blending=blending, top_k=16),
+                     planes=False)["counters"]
+        assert rows[i, 2] == o["rn_total"] and rows[i, 3] == o["rn_per_tile"] and rows[i, 4] == o["blended_total"]
+    assert rows[2, 4] == rows[3, 4]  # test_raster.cpp:372-390
+
+
+def _pose_cameras(w, h):
+    """Non-identity poses: C5 trajectory views and an arbitrary Camera::make pose with translation."""
+    cams = trajectory_cameras(256, w, h, first=0, count=256)
+    picks = [cams[i] for i in (5, 64, 131, 250)]
+    # a yaw + roll about the street camera (keeps the scene in view), translated, off-centre principal point
+    a, b = 0.07, 0.05
+    yaw = np.array([[math.cos(a), 0, math.sin(a)], [0, 1, 0], [-math.sin(a), 0, math.cos(a)]])
+    roll = np.array([[math.cos(b), -math.sin(b), 0], [math.sin(b), math.cos(b), 0], [0, 0, 1]])
+    tilt = roll @ yaw
+    picks.append(Camera.make(tilt, np.array([0.3, -0.2, 1.7]), 0.75 * w, 0.8 * w, 0.47 * w, 0.53 * h, w, h, 0.1,
+                             200.0))
+    return picks
+
+
+@pytest.mark.parametrize("blending,k", [(Blending.TopK, 16), (Blending.Full, 16)])
+def test_oracle_is_reference_non_identity_poses(c0, blending, k):
+    s, f, lab, _, cam, rs = c0
+    for pc in _pose_cameras(256, 192):
+        assert_oracle_is_reference(rs, SceneMap(s, f), lab, pc, RasterConfig(blending=blending, top_k=k),
+                                   libm_too=False)
+
+
+def test_oracle_is_reference_100k_1280x720():
+    """>= 100k surfels at 1280x720 (C3 shape, density-normalised, 64-d features, K = 8), the street
+    camera and one trajectory pose."""
+    n, w, h = 100_000, 1280, 720
+    sc, _, cam = make_street_scene(StreetSpec(n_surfels=n, image_w=w, image_h=h, c_sem=64,
+                                              scale_mult=density_scale(n, w, h)), with_labels=False)
+    rs = R.RefScene(sc.surfels, sc.f_sem, None)
+    cfg = RasterConfig(binning=Binning.Aabb, blending=Blending.TopK, top_k=8)
+    for c in (cam, trajectory_cameras(256, w, h, first=77, count=1)[0]):
+        assert_oracle_is_reference(rs, sc, None, c, cfg, libm_too=False)
+    rs.close()
+
+
+def test_stage_functions_are_reference():
+    """project_surfel, evaluate_alpha (raster.cpp:94-177) and topk_select (raster.cpp:225-251)."""
+    rng = Rng(5)
+    cams = _pose_cameras(320, 240)
+    cfg = RasterConfig()
+    for i in range(400):
+        c = cams[i % len(cams)]
+        q = rng.unit_quaternion()
+        s13 = np.array([rng.uniform(-3, 3), rng.uniform(-2, 2), rng.uniform(-1, 25), *q, rng.uniform(0.01, 1.5),
+                        rng.uniform(0.01, 0.4), rng.uniform(0.1, 1), 0.5, 0.5, 0.5])
+        pr, po = R.project_surfel(s13, c, cfg), O.project_surfel(s13, c, cfg.chi2)
+        assert (pr is None) == (po is None)
+        if pr is not None:
+            for k in pr:
+                assert np.array_equal(np.asarray(pr[k]), np.asarray(po[k])), k
+            for _ in range(4):
+                px, py = pr["center"] + np.array([rng.uniform(-6, 6), rng.uniform(-6, 6)])
+                px, py = math.floor(px) + 0.5, math.floor(py) + 0.5
+                ar, ao = R.evaluate_alpha(s13, c, px, py, cfg), O.evaluate_alpha(s13, c, px, py, cfg)
+                assert ar == ao
+    for m in (1, 5, 9, 40):
+        for k in (1, 4, 8, 16):
+            w = np.array([rng.uniform() for _ in range(m)])
+            w[: m // 3] = w[0]  # ties broken by proj ascending
+            p = np.array([int(rng.uniform_int(1000)) for _ in range(m)], np.int32)
+            assert np.array_equal(R.topk_select(w, p, k), O.topk_select(w, p, k))
