@@ -113,16 +113,22 @@ def build_workload(name, rank, world):
     scene, _, cam0 = make_street_scene(spec, with_labels=False)
     if name == "c3p":  # the panoptic layer's inputs: Surfel::f_ins and synthetic instance queries
         scene = SceneMap(scene.surfels, scene.f_sem, street_f_ins(spec), street_queries(C3P_QUERIES))
-    if name == "c5":
-        # the rank's contiguous block of the closed-form 256-view trajectory
-        from paper_2604_10982_b200.multiview import shard_range
-        views = list(shard_range(C5_VIEWS, world, rank))
-        cams = trajectory_cameras(C5_VIEWS, w, h, first=views[0], count=len(views)) if views else []
-    else:
-        # weak scaling: rank r renders trajectory view r (view 0 == the street camera)
-        cams = [cam0 if rank == 0 else trajectory_cameras(1, w, h, first=rank, count=1)[0]]
+    cams, _ = rank_cameras(name, cam0, rank, world)
     log(f"[rank {rank}] workload {name}: {len(scene)} surfels generated in {time.perf_counter() - t0:.1f}s")
     return scene, cams, (n, w, h, c, blending, k, desc)
+
+
+def rank_cameras(name, cam0, rank, world):
+    """The views rank `rank` of `world` renders each step, and their trajectory indices.
+    c5: the rank's contiguous block of the closed-form 256-view trajectory.
+    Other workloads (weak scaling): rank r renders trajectory view r (view 0 is the street camera)."""
+    from paper_2604_10982_b200 import trajectory_cameras
+    from paper_2604_10982_b200.multiview import shard_range
+    _, w, h = WORKLOADS[name][:3]
+    if name == "c5":
+        views = list(shard_range(C5_VIEWS, world, rank))
+        return (trajectory_cameras(C5_VIEWS, w, h, first=views[0], count=len(views)) if views else []), views
+    return [cam0 if rank == 0 else trajectory_cameras(1, w, h, first=rank, count=1)[0]], [rank]
 
 
 def raster_cfg(blending, k, reference=False):
@@ -133,43 +139,104 @@ def raster_cfg(blending, k, reference=False):
                         blending=Blending.TopK if blending == "topk" else Blending.Full, top_k=k)
 
 
-def cpu_reference(scene, cam, cfg, frames):
-    """The reference algorithm on the host cores: the oracle built with glibc exp (the reference's libm),
-    serial project + bin, std::thread tile loop (raster.cpp:297-504). Returns (frames/s, threads, sample)."""
+def reference_workload(name):
+    """The reference arm's inputs, built without the product library: the oracle's restatement of
+    make_street_scene (+ scale_mult), pinned bit-exact to the reference's own generator by
+    tests/test_ref_pin.py. Returns (surfels13, f_sem, psm_camera, (n, w, h, c, blending, k, desc))."""
     from oracle import pyoracle as O
-    times = []
-    for _ in range(frames):
-        t0 = time.perf_counter()
-        if scene.queries:  # render_panoptic (metrics.cpp:339-369): assign_labels + render + epilogue
-            O.render_panoptic(scene, scene.f_ins, scene.queries, cam, cfg)
+    from paper_2604_10982_b200.scene import StreetSpec, density_scale  # plain dataclass + formula
+    n, w, h, c, blending, k, desc = WORKLOADS[name]
+    t0 = time.perf_counter()
+    spec = StreetSpec(n_surfels=n, image_w=w, image_h=h, c_sem=c, scale_mult=density_scale(n, w, h))
+    if name == "c3p":
+        s, f, _, cam, fi = O.make_street_scene(spec, with_f_ins=True)
+    else:
+        s, f, _, cam = O.make_street_scene(spec)
+        fi = None
+    log(f"[reference] workload {name}: {s.shape[0]} surfels generated by the oracle in {time.perf_counter() - t0:.1f}s")
+    return s, f, fi, cam, (n, w, h, c, blending, k, desc)
+
+
+def repo_libs():
+    """The repo's shared libraries mapped into this process (evidence of what a timed arm ran)."""
+    try:
+        return sorted({ln.split()[-1].replace(ROOT + "/", "") for ln in open("/proc/self/maps")
+                       if ln.rstrip().endswith(".so") and ROOT in ln})
+    except OSError:
+        return []
+
+
+class CpuReference:
+    """The reference CPU renderer on the host cores. Preferred: oracle/_ref, the reference's own
+    raster.cpp / math_util.cpp / core_types.cpp compiled unchanged (kind "reference"): render_into
+    into persistent targets, serial project + bin, std::thread tile loop (raster.cpp:273-511), glibc exp.
+    For render_panoptic (c3p; panoptic.cpp / metrics.cpp are not compiled into _ref) and where _ref is
+    absent: the oracle restatement built with glibc exp (kind "port")."""
+
+    def __init__(self, surfels, f_sem, f_ins=None, queries=None):
+        from oracle import pyref as R
+        self.queries = queries
+        self.kind = "reference" if (R.available() and not queries) else "port"
+        if self.kind == "reference":
+            self.rs = R.RefScene(surfels, f_sem, None)
         else:
-            O.render(scene, None, cam, cfg, planes=False, libm=True)
-        times.append(time.perf_counter() - t0)
-    threads = int(os.environ.get("PSIMAP_THREADS", 0)) or os.cpu_count()
-    return 1.0 / min(times), threads, times
+            from paper_2604_10982_b200.raster import SceneMap
+            self.scene = SceneMap(surfels, f_sem, f_ins, queries)
+
+    def frame(self, cam_c, cfg):
+        if self.kind == "reference":
+            self.rs.render_into(cam_c, cfg.to_c())
+            return
+        from oracle import pyoracle as O
+        from paper_2604_10982_b200.raster import Camera
+        cam = Camera.from_c(cam_c)
+        if self.queries:  # render_panoptic (metrics.cpp:339-369): assign_labels + render + epilogue
+            O.render_panoptic(self.scene, self.scene.f_ins, self.queries, cam, cfg)
+        else:
+            O.render(self.scene, None, cam, cfg, planes=False, libm=True)
+
+    def time(self, cam_c, cfg, frames):
+        times = []
+        for _ in range(frames):
+            t0 = time.perf_counter()
+            self.frame(cam_c, cfg)
+            times.append(time.perf_counter() - t0)
+        return times
+
+    def describe(self, frames, w, h, n, threads):
+        what = ("the reference's raster.cpp/math_util.cpp/core_types.cpp compiled unchanged (oracle/_ref, "
+                "minimal Eigen stand-in), render_into into persistent targets" if self.kind == "reference" else
+                "reference algorithm restated in C++ (oracle), glibc exp")
+        return (f"{frames} full {w}x{h} frames of {n} surfels, best-of; {what}; serial project+bin, "
+                f"{threads} std::threads over tiles")
 
 
 def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
         return 0
-    scene, cams, (n, w, h, c, blending, k, desc) = build_workload(args.workload, 0, 1)
-    cam = cams[0]
+    s, f, fi, cam_c, (n, w, h, c, blending, k, desc) = reference_workload(args.workload)
+    queries = None
+    if args.workload == "c3p":
+        from paper_2604_10982_b200.panoptic import street_queries
+        queries = street_queries(C3P_QUERIES)
+    ref = CpuReference(s, f, fi, queries)
     cfg = raster_cfg(blending, k, reference=True)
-    for _ in range(args.warmup):
-        cpu_reference(scene, cam, cfg, 1)
-    fps, threads, times = cpu_reference(scene, cam, cfg, args.steps)
+    ref.time(cam_c, cfg, args.warmup)
+    times = ref.time(cam_c, cfg, args.steps)
+    fps = 1.0 / min(times)
+    threads = int(os.environ.get("PSIMAP_THREADS", 0)) or os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.mean(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: {desc}", "binning": "aabb (reference full_method)",
-                   "cpu_only": True},
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full {w}x{h} frames of {n} surfels, best-of (reference "
-                                   f"algorithm restated in C++, glibc exp, serial project+bin, "
-                                   f"{threads} std::threads over tiles)"},
+                   "cpu_only": True, "same_config_note": "AABB here vs Ellipse on the GPU: identical planes "
+                   "(tests/test_gpu_parity.py::test_gpu_c3_binning_output_identity)"},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": ref.kind,
+                         "sample": ref.describe(args.steps, w, h, n, threads)},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "libs_loaded": repo_libs(),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -360,15 +427,18 @@ def run_ours(args):
     # CPU baseline on rank 0 at N=1: the reference algorithm on the host cores, bounded sample
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        fps_cpu, threads, times = cpu_reference(scene, cam, raster_cfg(blending, k, reference=True), 2)
-        cpu = {"value": fps_cpu, "unit": "frames/s", "cores": threads, "kind": "port",
-               "sample": f"2 full {w}x{h} frames of {n} surfels (aabb + top-k), best-of; oracle built with glibc exp "
-                         f"(reference algorithm: serial project+bin, {threads} std::threads over tiles)"}
+        ref = CpuReference(scene.surfels, scene.f_sem, scene.f_ins, scene.queries or None)
+        times = ref.time(cam.to_c(), raster_cfg(blending, k, reference=True), 2)
+        threads = int(os.environ.get("PSIMAP_THREADS", 0)) or os.cpu_count()
+        cpu = {"value": 1.0 / min(times), "unit": "frames/s", "cores": threads, "kind": ref.kind,
+               "sample": ref.describe(2, w, h, n, threads)}
 
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64-decisions/f32-accum", "data": "synthetic",
+        "dtype_note": "projection, culling, binning, sort keys, support/alpha/transmittance and Top-K decisions in "
+                      "fp64 (bit-exact with the reference); colour/normal/feature sums in fp32 (1e-4 tolerance)",
         "config": {"workload": f"{args.workload}: {desc}", "binning": "ellipse (precise tile intersection)",
                    "queries": len(scene.queries), "assign_labels_ms": assign_ms,
                    "blending": blending, "top_k": k, "surfels": n, "n_proj": n_proj, "width": w, "height": h,
@@ -389,6 +459,7 @@ def run_ours(args):
                              + ("; c5: one psm_render_batch per step, views alternating over two streams"
                                 if batch else ""),
         "clocks": clk.summary(),
+        "libs_loaded": repo_libs(),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -422,6 +493,59 @@ def run_grid(args):
     return 0
 
 
+def spawn_ranks(args):
+    """`--gpus N` without a torchrun environment: re-launch this command as N ranks (one process
+    per GPU) under torch.distributed.run, exactly as the driver's multi-GPU launch does."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"spawning {args.gpus} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing of run_ours on CPU (gloo), without a device: process group,
+    per-rank views, barrier, per-rank step timing, MAX over ranks, one JSON line from rank 0. Frames are
+    not rendered (no GPU); used by tests/test_bench_ranks.py to exercise `--gpus N` end to end."""
+    import torch
+    import torch.distributed as dist
+    rank, _, world = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    from paper_2604_10982_b200 import Camera
+    n, w, h, c, blending, k, desc = WORKLOADS[args.workload]
+    cam0 = Camera.look_at((0, 0, 0), (0, 0, 20), (0, -1, 0), 0.8 * w, 0.8 * w, w, h, 0.1, 200.0)
+    cams, views = rank_cameras(args.workload, cam0, rank, world)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for cv in cams:
+            cv.to_c()  # the per-view kernel arguments; no render without a device
+    total_ms = (time.perf_counter() - t0) * 1000.0
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        gathered = [None] * world
+        dist.all_gather_object(gathered, {"rank": rank, "views": views,
+                                          "t_cw": [[float(x) for x in cv.t_cw] for cv in cams[:1]]})
+    else:
+        gathered = [{"rank": 0, "views": views}]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": total_ms / max(args.steps, 1),
+                          "config": {"workload": f"{args.workload}: {desc}"}, "ranks": gathered}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -431,7 +555,16 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", action="store_true", help="print the bench_render ablation grid instead")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing on CPU (gloo), no device work")
     args = ap.parse_args()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1 and args.impl == "ours" and not args.grid:
+        return spawn_ranks(args)
+    if env_world is not None and args.impl == "ours" and int(env_world) != args.gpus:
+        log(f"WORLD_SIZE={env_world} does not match --gpus {args.gpus}")
+        return 2
+    if args.dry_run:
+        return run_dry(args)
     if args.grid:
         return run_grid(args)
     if args.impl == "reference":

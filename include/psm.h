@@ -158,6 +158,9 @@ int psm_sync(psm_ctx* ctx);
  * bit-exact decisions; features and labels are stored fp32. */
 int psm_scene_upload(psm_ctx* ctx, const double* surfels13, int64_t n, const double* f_sem,
                      int32_t c_sem, const double* labels, int32_t n_q, psm_scene** out);
+/* psm_scene_free first settles ctx's pending asynchronous frames (psm_sync semantics), which
+ * may still read the scene; frames pending on other contexts must be synchronised by the caller.
+ * psm_assign_labels likewise settles ctx's pending frames before it rewrites the labels. */
 int psm_scene_free(psm_ctx* ctx, psm_scene* scene);
 int psm_scene_info(const psm_scene* scene, int64_t* n, int32_t* c_sem, int32_t* n_q);
 

@@ -198,7 +198,7 @@ __device__ __forceinline__ int key_shift(const unsigned long long* __restrict__ 
   return sh > 0 ? sh : 0;
 }
 
-__device__ __forceinline__ uint64_t sort_key(uint64_t bits, uint32_t src, uint64_t min_bits, int sh, int src_bits) {
+__device__ __forceinline__ uint64_t sort_key(uint64_t bits, uint64_t src, uint64_t min_bits, int sh, int src_bits) {
   return (((bits - min_bits) >> sh) << src_bits) | src;
 }
 
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(32 * kEmitWarps, PSM_EMIT_MINB) emit_kernel(co
       EmitItem& it = items[warp][lane];
       // the key's source field is (source << 8 | block mask), kFieldExtra bits wider than the source
       const int fb = src_bits + kFieldExtra;
-      it.key = sort_key(depth_bits[i], static_cast<uint32_t>(i) << kFieldExtra, depth_minmax[0],
+      it.key = sort_key(depth_bits[i], static_cast<uint64_t>(i) << kFieldExtra, depth_minmax[0],
                         key_shift(depth_minmax, fb), fb);
       if (ellipse || masks_on) {
         it.e = psm_ellipse_prep(recs[i].cx, recs[i].cy, b.F00, b.F01, b.F11, rs.chi2);

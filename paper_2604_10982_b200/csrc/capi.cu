@@ -504,6 +504,9 @@ int render_common(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, cons
   const psm_targets* tg = pt ? &scratch_only : tg_in;
   if (!ctx || !sc || !cam || !cfg || !tg) return fail(ctx, PSM_EINVAL, "null argument");
   if (cam->width <= 0 || cam->height <= 0) return fail(ctx, PSM_EINVAL, "camera: image size must be positive");
+  // Camera::make's invariant (core_types.cpp:23-25); the depth keys order positive depths only
+  if (!(cam->near_clip > 0) || !(cam->near_clip < cam->far_clip))
+    return fail(ctx, PSM_EINVAL, "camera: require 0 < near < far");
   PSM_TRY(check_config(ctx, cfg, sc->c_sem + sc->n_q));
   PSM_CUDA_TRY(cudaSetDevice(ctx->device));
   const size_t npx = static_cast<size_t>(cam->width) * cam->height;
@@ -831,6 +834,10 @@ int psm_assign_labels(psm_ctx* ctx, psm_scene* sc, const psm_queries* qs, double
     return fail(ctx, PSM_EINVAL, "feature_similarity: dimension mismatch");  // panoptic.cpp:12-14
   if (sc->c_sem + nq > 512) return fail(ctx, PSM_EUNSUPPORTED, "GPU path supports C_sem + N_q <= 512");
   PSM_CUDA_TRY(cudaSetDevice(ctx->device));
+  // asynchronous frames still pending on this context (or its batch twin) may be re-rendered
+  // at psm_sync against this scene: settle them before its labels change
+  PSM_TRY(psm::drain_twin(ctx));
+  if (!ctx->pend.empty()) PSM_TRY(psm::sync_impl(ctx));
   const int64_t n = sc->n;
   const int c_ins = qs->c_ins;
   // alive queries and their inverse covariances (panoptic.cpp:44-62), host side, once
@@ -1035,8 +1042,11 @@ int psm_render_panoptic(psm_ctx* ctx, const psm_scene* scene, const psm_camera* 
 }
 
 int psm_scene_free(psm_ctx* ctx, psm_scene* sc) {
-  (void)ctx;
   if (!sc) return PSM_OK;
+  if (ctx) {  // settle this context's pending asynchronous frames, which may still reference the scene
+    PSM_TRY(psm::drain_twin(ctx));
+    if (!ctx->pend.empty()) PSM_TRY(psm::sync_impl(ctx));
+  }
   cudaSetDevice(sc->device);
   if (sc->surfels) cudaFree(sc->surfels);
   if (sc->feat) cudaFree(sc->feat);

@@ -13,4 +13,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python profiles/frame.py c3 2 > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -o gpurun_out/${tag}_frame_full -f \
     python profiles/frame.py c3 2 > gpurun_out/${tag}_full.log 2>&1
+python profiles/summarize.py full gpurun_out/${tag}_frame_full.ncu-rep gpurun_out/${tag}_c3_kernels_ncu.json
+python profiles/summarize.py launches gpurun_out/${tag}_launches_frame.csv gpurun_out/${tag}_launches_c3_frame.csv
+python profiles/summarize.py launches gpurun_out/${tag}_launches_bench.csv gpurun_out/${tag}_launches_c3_bench.csv
+# bench.py's roofline.traffic comes from this same capture
+python profiles/summarize.py traffic gpurun_out/${tag}_c3_kernels_ncu.json profiles/blend_traffic.json
+cp profiles/blend_traffic.json gpurun_out/${tag}_blend_traffic.json
 echo captured

@@ -2,6 +2,7 @@
 
   python profiles/summarize.py full REPORT.ncu-rep OUT.json     # one entry per kernel launch (--set full)
   python profiles/summarize.py launches LAUNCHES.csv OUT.csv    # gpu__time_duration.sum launch list -> per-kernel shares
+  python profiles/summarize.py traffic SUMMARY.json OUT.json     # blend launch's DRAM bytes -> bench.py roofline.traffic
 
 The launch list is cold-cache and serialised (ncu replays each launch alone), so only
 each kernel's SHARE of the frame is comparable with bench.py, not the absolute time.
@@ -72,5 +73,23 @@ def launches(csv_in, out):
     print(f"{out}: {len(agg)} kernels, {tot:.1f} us")
 
 
+def traffic(summary_json, out):
+    """The last blend_kernel launch of a `full` summary (one frame's K7) -> the per-launch DRAM
+    traffic that bench.py reports as roofline.traffic."""
+    ents = [e for e in json.load(open(summary_json)) if e["kernel"].startswith(("blend_kernel", "void psm::blend"))
+            or "blend_kernel" in e["kernel"]]
+    if not ents:
+        raise SystemExit("no blend_kernel launch in " + summary_json)
+    e = ents[-1]
+    rd, wr = e["dram__bytes_read.sum"][0], e["dram__bytes_write.sum"][0]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    rd *= scale.get(e["dram__bytes_read.sum"][1], 1)
+    wr *= scale.get(e["dram__bytes_write.sum"][1], 1)
+    json.dump({"kernel": e["kernel"], "source": summary_json + " (ncu --set full --clock-control none, "
+               "python profiles/frame.py c3 2; profiles/capture.sh)", "dram_bytes_read": rd, "dram_bytes_write": wr,
+               "dram_bytes_per_launch": rd + wr, "launch_us": e["gpu__time_duration.sum"]}, open(out, "w"), indent=1)
+    print(f"{out}: {rd + wr:.0f} B per launch")
+
+
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"full": full, "launches": launches, "traffic": traffic}[sys.argv[1]](sys.argv[2], sys.argv[3])

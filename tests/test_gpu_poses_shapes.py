@@ -1,0 +1,133 @@
+"""GPU parity under non-identity camera poses and at the north-star's large shapes.
+
+The oracle is bit-identical to the reference's own compiled code (tests/test_ref_pin.py), so
+these compare the sm_100a path with the reference's results:
+  * C5 trajectory views and an arbitrary Camera::make pose with translation,
+    rotation about two axes and an off-centre principal point: the camera transform
+    products of project_surfel (raster.cpp:96-101) and center_world (core_types.hpp:52) are
+    no longer exact, so keys, lists, ranges, depth order and Top-K sets test them bit for bit;
+  * the C4/C5 shape (1920x1080, 128-d features, K = 16, Ellipse binning) at full size (5M
+    surfels), which runs the D = 128 exact feature instantiation and the fp32 warp-block mask
+    margins at 1920-px coordinates;
+  * the other exact feature shapes (D = 96, 256) and odd D around them.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2604_10982_b200 import (Binning, Blending, Camera, RasterConfig, Renderer, StreetSpec, density_scale,
+                                   make_street_scene, trajectory_cameras)
+from tests.test_gpu_parity import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rend():
+    r = Renderer(0)
+    yield r
+    r.close()
+
+
+def make_pose(w, h):
+    """Camera::make with yaw 0.07 and roll 0.05 rad, translation (0.3, -0.2, 1.7), fx != fy and an
+    off-centre principal point."""
+    a, b = 0.07, 0.05
+    yaw = np.array([[math.cos(a), 0, math.sin(a)], [0, 1, 0], [-math.sin(a), 0, math.cos(a)]])
+    roll = np.array([[math.cos(b), -math.sin(b), 0], [math.sin(b), math.cos(b), 0], [0, 0, 1]])
+    return Camera.make(roll @ yaw, np.array([0.3, -0.2, 1.7]), 0.75 * w, 0.8 * w, 0.47 * w, 0.53 * h, w, h, 0.1,
+                       200.0)
+
+
+def street(n, w, h, c_sem, labels=False, n_instances=256):
+    return make_street_scene(StreetSpec(n_surfels=n, image_w=w, image_h=h, c_sem=c_sem, n_instances=n_instances,
+                                        scale_mult=density_scale(n, w, h)), with_labels=labels)
+
+
+@pytest.mark.parametrize("binning,blending,k", [(Binning.Ellipse, Blending.TopK, 8), (Binning.Circle, Blending.Full, 16),
+                                                (Binning.Aabb, Blending.TopK, 16)])
+def test_gpu_trajectory_poses(rend, binning, blending, k):
+    """Four C5 trajectory views and the Camera::make pose on a 60k-surfel 640x360 street scene."""
+    sc, _, _ = street(60_000, 640, 360, 32)
+    cams = [trajectory_cameras(256, 640, 360, first=i, count=1)[0] for i in (5, 64, 131, 250)]
+    for cam in cams + [make_pose(640, 360)]:
+        g, _ = assert_parity(rend, sc, None, cam, RasterConfig(binning=binning, blending=blending, top_k=k))
+        assert g.blended_total > 0
+
+
+def test_gpu_trajectory_labels(rend):
+    """Labels (N_q = 24) under a trajectory view and the make pose."""
+    sc, labels, _ = street(20_000, 320, 180, 16, labels=True, n_instances=24)
+    for cam in (trajectory_cameras(256, 320, 180, first=200, count=1)[0], make_pose(320, 180)):
+        assert_parity(rend, sc, labels, cam, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=8))
+
+
+def test_gpu_c3_trajectory_full_size(rend):
+    """Full C3 (1M surfels, 1280x720, 64-d, K = 8) from two trajectory views and the make pose."""
+    sc, _, _ = street(1_000_000, 1280, 720, 64)
+    cfg = RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=8)
+    for cam in trajectory_cameras(256, 1280, 720, first=96, count=1) + [make_pose(1280, 720)]:
+        g, _ = assert_parity(rend, sc, None, cam, cfg)
+        assert g.rn_total > 500_000
+
+
+@pytest.fixture(scope="module")
+def c4():
+    return street(5_000_000, 1920, 1080, 128)
+
+
+def test_gpu_c4_full_size_parity(rend, c4):
+    """C4: 5M surfels, 1920x1080, 128-d features, K = 16, Ellipse binning, the street camera: every
+    bit-exact artefact (keys, lists, ranges, depth order, Top-K sets, counts, counters) and every plane."""
+    sc, _, cam = c4
+    g, _ = assert_parity(rend, sc, None, cam, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=16))
+    assert g.rn_total > 5_000_000 and g.n_proj > 4_000_000
+
+
+def test_gpu_c5_view_full_size_parity(rend, c4):
+    """A C5 trajectory view (view 160 of 256) over the full 5M-surfel scene."""
+    sc, _, _ = c4
+    cam = trajectory_cameras(256, 1920, 1080, first=160, count=1)[0]
+    assert_parity(rend, sc, None, cam, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=16))
+
+
+@pytest.mark.parametrize("c_sem", [96, 128, 256, 100, 127, 129, 200])
+@pytest.mark.parametrize("k", [8, 16])
+def test_gpu_feature_shapes(rend, c_sem, k):
+    """Exact-shape feature instantiations (D = 96, 128, 256) and the generic paths around them."""
+    sc, _, cam = street(8_000, 256, 144, c_sem)
+    for c in (cam, make_pose(256, 144)):
+        assert_parity(rend, sc, None, c, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=k))
+    assert_parity(rend, sc, None, cam, RasterConfig(binning=Binning.Aabb, blending=Blending.Full))
+
+
+def test_gpu_source_ids_beyond_2_24(rend):
+    """Surfel indices >= 2^24: the sort keys carry (source << 8 | block mask) in 64 bits, so the
+    tile lists still name the right surfels (reference indices are int, raster.cpp:302)."""
+    from tests.helpers import facing_surfel, front_camera
+    from paper_2604_10982_b200 import SceneMap
+    n_hidden = (1 << 24) + 5
+    rows = np.zeros((n_hidden + 48, 13))
+    rows[:n_hidden] = facing_surfel((0, 0, -5), 0.2, 0.2, 1.0, (1, 1, 1))  # behind the camera: culled
+    rng = np.random.default_rng(4)
+    for j in range(48):
+        rows[n_hidden + j] = facing_surfel((rng.uniform(-0.6, 0.6), rng.uniform(-0.4, 0.4), rng.uniform(1.5, 4)),
+                                           rng.uniform(0.05, 0.2), rng.uniform(0.05, 0.2), rng.uniform(0.3, 0.9),
+                                           tuple(rng.uniform(0, 1, 3)))
+    sc = SceneMap(rows, np.tile(np.arange(3.0), (rows.shape[0], 1)))
+    g, o = assert_parity(rend, sc, None, front_camera(96, 64), RasterConfig(binning=Binning.Ellipse,
+                                                                            blending=Blending.TopK, top_k=4))
+    assert g.n_proj == 48 and g.blended_total > 0
+
+
+def test_gpu_camera_clip_planes_validated(rend):
+    """0 < near < far (Camera::make, core_types.cpp:23-25) is required of every camera."""
+    from tests.helpers import facing_surfel, front_camera
+    from paper_2604_10982_b200 import SceneMap
+    sc = SceneMap(np.array([facing_surfel((0, 0, 2), 0.2, 0.2, 1.0, (1, 1, 1))]))
+    for near, far in ((0.0, 100.0), (-1.0, 100.0), (5.0, 5.0), (float("nan"), 100.0)):
+        cam = front_camera()
+        cam.near_clip, cam.far_clip = near, far
+        with pytest.raises(ValueError):
+            rend.render(sc, None, cam, RasterConfig())
