@@ -64,14 +64,8 @@ constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
 #ifndef PSM_BLEND_MB32
 #define PSM_BLEND_MB32 2
 #endif
-// candidate records per alpha-phase iteration (independent fp64 chains in flight)
-#ifndef PSM_BLEND_PER
-#define PSM_BLEND_PER 1
-#endif
-// lanes that walk one need mask together: 1, 2 (the default: two horizontally adjacent
-// pixels), 4 (a 4x1 row), 8 (4x2) or 16 (4x4). C3 blend: 0.812 / 0.809 / 0.834 / 0.841 / 0.875 ms
-#ifndef PSM_BLEND_GROUP
-#define PSM_BLEND_GROUP 2
+#ifndef PSM_BLEND_CH0
+#define PSM_BLEND_CH0 30
 #endif
 #ifndef PSM_BLEND_W8
 #define PSM_BLEND_W8 8
@@ -82,13 +76,23 @@ constexpr int kRecVec = sizeof(SurfRec) / 16;  // 9
 #ifndef PSM_BLEND_W32
 #define PSM_BLEND_W32 8
 #endif
+// candidate records per alpha-phase iteration
+#ifndef PSM_BLEND_PER
+#define PSM_BLEND_PER 1
+#endif
+// lanes that walk one need mask together: 1, 2 (the default: two
+// horizontally adjacent pixels), 4 (a 4x1 row), 8 (4x2) or 16 (4x4). C3 blend:
+// 0.812 / 0.809 / 0.834 / 0.841 / 0.875 ms
+#ifndef PSM_BLEND_GROUP
+#define PSM_BLEND_GROUP 2
+#endif
 // warps per CTA (each pulls its own work items; the count only sets residency and registers)
 __host__ __device__ constexpr int cta_warps(int kmax) {
   return kmax == 0 ? 8 : (kmax <= 8 ? PSM_BLEND_W8 : (kmax <= 16 ? PSM_BLEND_W16 : PSM_BLEND_W32));
 }
 __host__ __device__ constexpr int cta_threads(int kmax) { return 32 * cta_warps(kmax); }
 __host__ __device__ constexpr int chunk_for(int kmax) {
-  return kmax == 0 ? 30 : (kmax <= 8 ? PSM_BLEND_CH8 : (kmax <= 16 ? PSM_BLEND_CH16 : PSM_BLEND_CH32));
+  return kmax == 0 ? PSM_BLEND_CH0 : (kmax <= 8 ? PSM_BLEND_CH8 : (kmax <= 16 ? PSM_BLEND_CH16 : PSM_BLEND_CH32));
 }
 __host__ __device__ constexpr int min_blocks(int kmax) {
   return kmax == 0 ? 3 : (kmax <= 8 ? PSM_BLEND_MB8 : (kmax <= 16 ? PSM_BLEND_MB16 : PSM_BLEND_MB32));
@@ -101,9 +105,20 @@ __device__ unsigned long long psm_blend_stats[16];
 #endif
 
 constexpr size_t kExpTabBytes = 256 * sizeof(uint64_t);
+__host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) / 16 * 16; }
+// Staging copies: PSM_BLEND_TMA = 0 (the default): nine 16 B cp.async per 144 B record,
+// issued by the lane that found the entry; 1: one bulk copy (cp.async.bulk through the TMA
+// unit) per record, completing on the buffer's mbarrier (expect_tx per record, one arrival
+// per chunk). Measured (r02g, C3 blend): 0.806 ms with cp.async vs 0.854 ms with bulk
+// copies (C4 2.97 vs 3.16 ms): the records are gathered by source id, so each bulk copy
+// moves only 144 B, and the per-copy mbarrier traffic outweighs the 8 LDGSTS it saves.
+#ifndef PSM_BLEND_TMA
+#define PSM_BLEND_TMA 0
+#endif
 // per warp: [2][chunk] staged records + [2][chunk] their list positions (16 B aligned)
+// + the two buffers' mbarriers
 __host__ __device__ constexpr size_t warp_stage_bytes(int kmax) {
-  return (2 * chunk_for(kmax) * (sizeof(SurfRec) + sizeof(int)) + 15) / 16 * 16;
+  return align16(2 * chunk_for(kmax) * (sizeof(SurfRec) + sizeof(int))) + 16;
 }
 __host__ __device__ constexpr size_t stage_bytes(int kmax) {
   return static_cast<size_t>(cta_warps(kmax)) * warp_stage_bytes(kmax);
@@ -111,9 +126,12 @@ __host__ __device__ constexpr size_t stage_bytes(int kmax) {
 __host__ __device__ constexpr size_t smem_bytes(int kmax) {
   return stage_bytes(kmax) + kExpTabBytes + static_cast<size_t>(kmax) * cta_threads(kmax) * (sizeof(double) + sizeof(int));
 }
+static_assert(smem_bytes(0) * 3 + 1024 * 3 <= 228 * 1024, "full-blend shape exceeds shared memory");
 static_assert(smem_bytes(8) * PSM_BLEND_MB8 + 1024 * PSM_BLEND_MB8 <= 228 * 1024, "K=8 shape exceeds shared memory");
 static_assert(smem_bytes(16) * PSM_BLEND_MB16 + 1024 * PSM_BLEND_MB16 <= 228 * 1024, "K=16 shape exceeds shared memory");
 static_assert(smem_bytes(32) * PSM_BLEND_MB32 + 1024 * PSM_BLEND_MB32 <= 228 * 1024, "K=32 shape exceeds shared memory");
+static_assert(PSM_BLEND_CH0 <= 32 && PSM_BLEND_CH8 <= 32 && PSM_BLEND_CH16 <= 32 && PSM_BLEND_CH32 <= 32,
+              "chunks are 32-bit masks");
 
 // before(a, b) of topk_select (raster.cpp:232-235), proj order == source order.
 // Slots hold list positions; the source ids are only looked up on an exact weight tie.
@@ -126,6 +144,27 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+// mbarrier + bulk-copy primitives (PTX ISA 8.0, sm_90+)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
@@ -173,7 +212,7 @@ __device__ __forceinline__ int blk_py(int q) { return (q >> 2) & 3; }
 // One warp's work item: the 8x4 pixel block `blk` (0..7) of tile `tile`; lane -> pixel.
 template <int KMAX, bool FULL_LIST, int VEC, int NV, int LPP, bool EXACT, int PANO_T>
 __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile, const int blk, SurfRec* stage,
-                                            const uint64_t* exp_tab, double* top_w, int* top_p) {
+                                            const uint64_t* exp_tab, double* top_w, int* top_p, unsigned& phase) {
   constexpr int kChunk = chunk_for(KMAX);
   constexpr int kCT = cta_threads(KMAX);  // Top-K column stride
   constexpr int kPer = PSM_BLEND_PER;     // candidate records evaluated per iteration
@@ -205,6 +244,8 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
 
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
   int* spos = reinterpret_cast<int*>(stage + 2 * kChunk);  // [2][kChunk] list positions of the staged records
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(stage) + warp_stage_bytes(KMAX) - 16);
+  unsigned pending = 0;  // buffers with a bulk-copy phase not yet waited on
   // The tile list is read in 32-entry windows (source id + warp-block mask per lane, the
   // next window's loads in flight); the entries whose mask has this warp's block bit
   // are compacted into chunks of kChunk staged records (cp.async by the owning lane).
@@ -240,16 +281,38 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       if (mine) {
         const char* g = reinterpret_cast<const char*>(p.recs + cv);
         char* d = reinterpret_cast<char*>(stage + bf * kChunk + filled + r);
+#if PSM_BLEND_TMA
+        mbar_expect_tx(bars + bf, sizeof(SurfRec));
+        bulk_copy_g2s(d, g, sizeof(SurfRec), bars + bf);
+#else
 #pragma unroll
         for (int k = 0; k < kRecVec; ++k) cp_async16(d + 16 * k, g + 16 * k);
+#endif
         spos[bf * kChunk + filled + r] = wb + lane;
       }
       filled += __popc(take);
       clive &= ~take;
       if (filled == kChunk) break;
     }
+#if PSM_BLEND_TMA
+    __syncwarp();  // every lane's expect_tx precedes the arrival that closes the phase
+    if (lane == 0) mbar_arrive(bars + bf);
+    pending |= 1u << bf;
+#else
     cp_async_commit();
+#endif
     return filled;
+  };
+  // waits until buffer bf's staged records have landed
+  auto land = [&](int bf) {
+#if PSM_BLEND_TMA
+    mbar_wait(bars + bf, (phase >> bf) & 1u);
+    phase ^= 1u << bf;
+    pending &= ~(1u << bf);
+#else
+    (void)bf;
+    cp_async_wait<1>();
+#endif
   };
 
 #ifdef PSM_BLEND_STATS
@@ -259,8 +322,8 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
   int buf = 0;
   while (cnt > 0) {
     if (__all_sync(0xffffffffu, done)) break;
-    const int ncnt = assemble(buf ^ 1);  // always commits one (possibly empty) group
-    cp_async_wait<1>();
+    const int ncnt = assemble(buf ^ 1);  // always commits one (possibly empty) group / phase
+    land(buf);
     __syncwarp();
     const SurfRec* recs = stage + buf * kChunk;
 #ifdef PSM_BLEND_STATS
@@ -424,7 +487,12 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     buf ^= 1;
     cnt = ncnt;
   }
+#if PSM_BLEND_TMA
+  for (int bf = 0; bf < 2; ++bf)  // drain: the staging is rewritten by the next item
+    if (pending >> bf & 1u) land(bf);
+#else
   cp_async_wait<0>();
+#endif
 #ifdef PSM_BLEND_STATS
   {
     unsigned mx = st_iter;
@@ -472,8 +540,9 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
           for (int i = 0; i < blend_n; ++i) p.topk_pos[pix * k_sel + i] = top_p[i * kCT + tid];
       }
     }
-    // ins_argmax stays -1 unless labels were accumulated (raster.cpp:292,497)
-    if (p.n_q == 0 || blend_n == 0 || NV == 0) p.ins_argmax[pix] = -1;
+    // ins_argmax stays -1 unless labels were accumulated (raster.cpp:292,497); the fp64
+    // feature phase (PANO_T > 0) writes it itself
+    if (PANO_T == 0 && (p.n_q == 0 || blend_n == 0 || NV == 0)) p.ins_argmax[pix] = -1;
   }
 
   // blended_total (raster.cpp:459,502,506): one atomic per warp
@@ -601,10 +670,13 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     }
   }
 
-  // ---- panoptic planes (render_panoptic, metrics.cpp:339-369), fused: features and
-  // labels are accumulated in fp64 over the selected entries in blend order, exactly as
-  // raster.cpp:456-499 does (first entry writes, later ones add; --fmad=false), so the
-  // argmaxes are the reference's; only the three int planes are written.
+  // ---- fp64 feature phase: features and labels are accumulated in fp64 over the selected
+  // entries in blend order, exactly as raster.cpp:456-499 does (first entry writes, later
+  // ones add; --fmad=false), so the argmaxes are the reference's. Two modes:
+  //  * render_panoptic (metrics.cpp:339-369, fused; p.planes64 == 0): only the three int
+  //    planes are written;
+  //  * render with labels (p.planes64 == 1): the sem_feat / ins_dist planes (the fp64 sums
+  //    rounded once to fp32) and the exact ins_argmax (raster.cpp:486-498).
   if constexpr (PANO_T > 0) {
     if constexpr (KMAX > 0) {  // selected entries back into blend (list position) order
       for (int i = 1; i < blend_n; ++i) {
@@ -622,7 +694,9 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     }
     __syncwarp();
     const int D = p.feat_dims, cs = p.c_sem;
-    const bool gate = inside && !(1.0 - T < 0.5);  // alpha_acc < 0.5 -> void (metrics.cpp:351)
+    const bool planes = p.planes64 != 0;
+    // panoptic: alpha_acc < 0.5 -> void (metrics.cpp:351); planes: every pixel of the image
+    const bool gate = inside && (planes || !(1.0 - T < 0.5));
     int nsel = blend_n;
     if constexpr (FULL_LIST) nsel = nsel < p.list_cap ? nsel : p.list_cap;
     for (int q = 0; q < 32; ++q) {
@@ -631,7 +705,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       const int nq = __shfl_sync(0xffffffffu, nsel, q);
       const int64_t qpix = static_cast<int64_t>(qy) * p.width + qx;
       if (!qgate) {
-        if (lane == 0 && qx < p.width && qy < p.height) {
+        if (lane == 0 && qx < p.width && qy < p.height && !planes) {
           p.pan_ids[qpix] = -1;
           p.pan_classes[qpix] = -1;
           p.pan_sem[qpix] = -1;
@@ -701,6 +775,20 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         if (oks != 0x7fffffff && (ks == 0x7fffffff || os > bs || (os == bs && oks < ks))) { bs = os; ks = oks; }
         if (oki != 0x7fffffff && (ki == 0x7fffffff || oi > bi || (oi == bi && oki < ki))) { bi = oi; ki = oki; }
       }
+      if (planes) {  // raster.cpp:486-498: zeros (and -1) where nothing blended
+#pragma unroll
+        for (int t = 0; t < PANO_T; ++t) {
+          const int c = lane + 32 * t;
+          const float v = nq > 0 ? static_cast<float>(acc[t]) : 0.f;
+          if (c < cs) {
+            if (p.sem_feat) p.sem_feat[qpix * cs + c] = v;
+          } else if (c < D) {
+            if (p.ins_dist) p.ins_dist[qpix * p.n_q + (c - cs)] = v;
+          }
+        }
+        if (lane == 0) p.ins_argmax[qpix] = (p.n_q > 0 && nq > 0) ? ki : -1;
+        continue;
+      }
       if (lane == 0) {
         // ins_argmax stays -1 without labels or blends (raster.cpp:292,497); the
         // semantic plane is all zeros when nothing blended, whose first max is 0
@@ -730,6 +818,15 @@ __global__ void __launch_bounds__(cta_threads(KMAX), min_blocks(KMAX)) blend_ker
   double* top_w = reinterpret_cast<double*>(exp_tab + 256);
   int* top_p = reinterpret_cast<int*>(top_w + KMAX * kCT);
   for (int i = threadIdx.x; i < 256; i += kCT) exp_tab[i] = psm_exp_tab_dev[i];
+  unsigned phase = 0;  // parity of each staging buffer's current mbarrier phase
+#if PSM_BLEND_TMA
+  if ((threadIdx.x & 31) == 0) {
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(stage) + warp_stage_bytes(KMAX) - 16);
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+#endif
   __syncthreads();
   const int n_items = p.n_tiles * kBlocks;
   for (;;) {
@@ -738,7 +835,8 @@ __global__ void __launch_bounds__(cta_threads(KMAX), min_blocks(KMAX)) blend_ker
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
     const int tile = p.order ? __ldg(p.order + item / kBlocks) : p.tile_base + item / kBlocks;
-    blend_block<KMAX, FULL_LIST, VEC, NV, LPP, EXACT, PANO_T>(p, tile, item % kBlocks, stage, exp_tab, top_w, top_p);
+    blend_block<KMAX, FULL_LIST, VEC, NV, LPP, EXACT, PANO_T>(p, tile, item % kBlocks, stage, exp_tab, top_w, top_p,
+                                                             phase);
     __syncwarp();  // the lanes' Top-K columns and staging are rewritten by the next item
   }
 }
@@ -827,7 +925,7 @@ void launch_blend(const BlendParams& p, int tiles, bool topk, cudaStream_t st) {
     else launch_t<32, true, 1, 0, 32, true>(p, tiles, st);
     return;
   }
-  if (p.pan_ids) {  // render_panoptic: fp64 blend-order feature phase and the three id planes
+  if (p.pan_ids || p.planes64) {  // render_panoptic / render with labels: the fp64 blend-order feature phase
     if (!topk) launch_pano<0, true>(p, tiles, st);
     else if (blend_kmax_for(p.k_sel) == 8) launch_pano<8, false>(p, tiles, st);
     else if (blend_kmax_for(p.k_sel) == 16) launch_pano<16, false>(p, tiles, st);

@@ -333,6 +333,12 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->topk_dbg, npx * k_sel, &tk));
     bp.topk_dbg = tk;
   }
+  // render with labels: the fp64 feature phase (exact ins_argmax) over the scene's fp64 rows
+  const bool planes64 = !pl.pan_ids && !pl.cache && sc->n_q > 0 && sc->feat64 != nullptr;
+  if (planes64) {
+    bp.planes64 = 1;
+    bp.feat64 = sc->feat64;
+  }
   const bool full_list = (!topk && feat_dims > 0) || pl.cache;
   if (full_list) {
     if (ctx->list_cap == 0) ctx->list_cap = 128;
@@ -340,7 +346,7 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
     PSM_TRY(ensure(ctx, ctx->lists, npx * ctx->list_cap, &lists));
     bp.lists = lists;
     bp.list_cap = ctx->list_cap;
-    if (pl.pan_ids) {
+    if (pl.pan_ids || planes64) {
       double* lw;
       PSM_TRY(ensure(ctx, ctx->lists_w, npx * ctx->list_cap, &lw));
       bp.lists_w = lw;
@@ -779,7 +785,9 @@ int psm_scene_create(psm_ctx* ctx, const psm_scene_desc* d, psm_scene** out) {
   sc->c_ins = c_ins;
   sc->flags = d->flags;
   const int D = c_sem + n_q;
-  const bool exact = (d->flags & PSM_SCENE_EXACT_FEATURES) != 0;
+  // fp64 rows are kept for PSM_SCENE_EXACT_FEATURES and whenever the scene has labels (the
+  // render's fp64 label phase gives the reference's ins_argmax exactly)
+  const bool exact = (d->flags & PSM_SCENE_EXACT_FEATURES) != 0 || n_q > 0;
   if (n > 0) {
     cudaError_t e = cudaMalloc(&sc->surfels, sizeof(double) * 13 * n);
     if (e == cudaSuccess) e = cudaMemcpy(sc->surfels, d->surfels13, sizeof(double) * 13 * n, cudaMemcpyHostToDevice);
@@ -859,7 +867,7 @@ int psm_assign_labels(psm_ctx* ctx, psm_scene* sc, const psm_queries* qs, double
     psm_query_inverse(qs->cov + q * 9, inv + a * 9);
   }
   const int D = sc->c_sem + nq;
-  const bool exact = sc->feat64 != nullptr || (sc->flags & PSM_SCENE_EXACT_FEATURES);
+  const bool exact = sc->feat64 != nullptr || (sc->flags & PSM_SCENE_EXACT_FEATURES) || nq > 0;
   cudaStream_t st = ctx->stream;
   // the rows are rewritten in place when the width is unchanged (each thread reads its
   // own row's f_sem columns before writing it); otherwise into new buffers

@@ -36,6 +36,9 @@ struct BlendParams {
   const double* feat64;   // [N][feat_dims] fp64
   double* lists_w;        // full blending: fp64 weights beside `lists`
   int32_t *pan_ids, *pan_classes, *pan_sem;
+  // render with labels (N_q > 0): the fp64 feature phase writes sem_feat / ins_dist /
+  // ins_argmax from feat64, so ins_argmax is the reference's exactly
+  int32_t planes64;
   const int32_t* query_class;
   int32_t n_query_class;
   // backward cache (RenderCache::pixels, raster.cpp:399-403): when lists_t != NULL the

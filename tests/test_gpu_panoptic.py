@@ -89,9 +89,15 @@ def test_gpu_render_panoptic_no_queries_and_no_features(rend, street):
 
 def test_gpu_render_panoptic_needs_exact_scene(rend, street):
     sc, cam = street
-    ds = rend.upload(sc, np.full((len(sc), 2), 0.5))
+    ds = rend.upload(sc)  # features, no labels, no PSM_SCENE_EXACT_FEATURES: fp32 rows only
     with pytest.raises(NotImplementedError):  # PSM_EUNSUPPORTED
         rend.render_panoptic(ds, cam, RasterConfig(), [0, 1])
+    # a scene with labels keeps its fp64 rows (the render's exact label phase), so it also serves render_panoptic
+    lab = np.tile(np.array([0.25, 0.75]), (len(sc), 1))
+    a = rend.render_panoptic(rend.upload(sc, lab), cam, RasterConfig(), [3, 4])
+    b = rend.render_panoptic(rend.upload(sc, lab, exact=True), cam, RasterConfig(), [3, 4])
+    for k in ("ids", "classes", "sem_classes"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
 
 
 def test_gpu_render_panoptic_c3p_full_size(rend):

@@ -73,14 +73,8 @@ def assert_parity(rend, scene, labels, cam, cfg, check_debug=True):
         if a.size:
             err = np.max(np.abs(a.astype(np.float64) - b))
             assert err <= ATOL, (k, err)
-    # ins_argmax: exact except where the oracle's top-2 label masses tie within fp32 accumulation noise
-    ga, oa = g.ins_argmax[..., 0], o["ins_argmax"][..., 0]
-    if o["ins_dist"].shape[-1] > 1:
-        srt = np.sort(o["ins_dist"], axis=-1)
-        near_tie = (srt[..., -1] - srt[..., -2]) < 1e-5
-        assert np.all((ga == oa) | near_tie)
-    else:
-        assert np.array_equal(ga, oa)
+    # ins_argmax: exact (labels blend in fp64 in blend order, raster.cpp:456-498)
+    assert np.array_equal(g.ins_argmax, o["ins_argmax"]), "ins_argmax"
     return g, o
 
 
@@ -300,3 +294,18 @@ def test_gpu_huge_buckets_and_depth_ties(rend, count):
     g, o = assert_parity(rend, sc, None, cam, RasterConfig(binning=Binning.Aabb, blending=Blending.TopK, top_k=8))
     tiles = O.bin_surfels(rows, cam, RasterConfig(), 1)["tiles"]
     assert max(len(t) for t in tiles) > (16384 if count > 16384 else 4096)
+
+
+def test_gpu_ins_argmax_below_fp32_resolution(rend):
+    """Label masses that differ only below fp32 resolution: the argmax follows the fp64 blend-order sums
+    (raster.cpp:486-498), including exact fp64 ties (first index wins)."""
+    sc, _, cam = make_street_scene(StreetSpec(n_surfels=2500, image_w=96, image_h=64, c_sem=5, n_instances=4))
+    n = len(sc)
+    rng = np.random.default_rng(11)
+    base = rng.uniform(0.1, 0.4, n)
+    labels = np.stack([base, base + 1e-12 * (1 + (np.arange(n) % 3)), base, rng.uniform(0, 0.05, n)], axis=1)
+    labels[::7, 1] = labels[::7, 0]  # exact ties on some surfels
+    for cfg in (RasterConfig(blending=Blending.TopK, top_k=8, binning=Binning.Ellipse),
+                RasterConfig(blending=Blending.Full)):
+        g, o = assert_parity(rend, sc, labels, cam, cfg)
+        assert np.count_nonzero(o["ins_argmax"] == 1) > 0

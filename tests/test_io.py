@@ -98,9 +98,8 @@ def test_cli_render_matches_oracle(street_ckpt):
                       ("ins_dist", "ins_dist"), ("alpha", "alpha_acc")):
         a = pio.load_raw(str(out / f"{name}.raw"))
         assert a.shape == o[key].shape and np.max(np.abs(a - o[key])) <= 1e-4, name
-    ga, oa = pio.load_raw(str(out / "ins_argmax.raw"))[..., 0], o["ins_argmax"][..., 0]
-    srt = np.sort(o["ins_dist"], axis=-1)
-    assert np.all((ga == oa) | ((srt[..., -1] - srt[..., -2]) < 1e-5))
+    # labels blend in fp64 in blend order on the GPU (raster.cpp:486-498): the argmax is exact
+    assert np.array_equal(pio.load_raw(str(out / "ins_argmax.raw"))[..., 0], o["ins_argmax"][..., 0])
     assert (out / "color.ppm").exists() and json.loads((out / "run_config.json").read_text())["topk"] == "8"
 
 
