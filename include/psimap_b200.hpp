@@ -13,8 +13,9 @@
 //
 // Every render runs on the GPU (libpsm.so); there is no CPU fallback. A degenerate
 // quaternion throws std::invalid_argument like rotation_from_quat
-// (math_util.cpp:48-50); other failures throw std::runtime_error. RenderCache is
-// not supported (backward is out of scope): passing one throws.
+// (math_util.cpp:48-50); other failures throw std::runtime_error. The stage functions
+// (project_surfel, bin_circle, bin_aabb, sample_surfel_alpha, evaluate_alpha, topk_select,
+// raster.hpp:87-126) and RenderCache (raster.hpp:76-82) run on the GPU too.
 //
 // Link: -I<repo>/include -L<repo>/paper_2604_10982_b200 -lpsm
 #ifndef PSIMAP_B200_HPP
@@ -26,6 +27,7 @@
 #include <cmath>
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -52,6 +54,12 @@ struct Mat3 {  // column-major like Eigen::Matrix3d
   double& operator()(int r, int c) { return m[c * 3 + r]; }
   double operator()(int r, int c) const { return m[c * 3 + r]; }
   static Mat3 Identity() { return Mat3{}; }
+};
+
+struct Mat2 {  // column-major like Eigen::Matrix2d
+  std::array<double, 4> m{{0, 0, 0, 0}};
+  double& operator()(int r, int c) { return m[c * 2 + r]; }
+  double operator()(int r, int c) const { return m[c * 2 + r]; }
 };
 
 struct VecX : std::vector<double> {  // Eigen::VectorXd stand-in
@@ -198,7 +206,77 @@ struct RenderTargets {  // raster.hpp:56-66
   uint64_t blended_total = 0;
 };
 
-struct RenderCache;  // backward-pass intermediates: out of scope on the GPU path
+struct ProjectedSurfel {  // raster.hpp:21-30
+  int source = -1;
+  Vec2 screen_center{};
+  Mat2 sigma{};
+  double sort_depth = 0;
+  Mat3 h = Mat3{{{0, 0, 0, 0, 0, 0, 0, 0, 0}}};
+  Mat3 h_inv = Mat3{{{0, 0, 0, 0, 0, 0, 0, 0, 0}}};
+  Mat2 footprint_inv{};
+  Vec3 normal_vis{{0, 0, 1}};
+
+  static ProjectedSurfel from_c(const psm_projected& p) {
+    ProjectedSurfel o;
+    o.source = p.source;
+    for (int i = 0; i < 2; ++i) o.screen_center[i] = p.screen_center[i];
+    std::copy(p.sigma, p.sigma + 4, o.sigma.m.begin());
+    o.sort_depth = p.sort_depth;
+    std::copy(p.h, p.h + 9, o.h.m.begin());
+    std::copy(p.h_inv, p.h_inv + 9, o.h_inv.m.begin());
+    std::copy(p.footprint_inv, p.footprint_inv + 4, o.footprint_inv.m.begin());
+    for (int i = 0; i < 3; ++i) o.normal_vis[i] = p.normal_vis[i];
+    return o;
+  }
+  psm_projected to_c() const {
+    psm_projected p{};
+    p.source = source;
+    for (int i = 0; i < 2; ++i) p.screen_center[i] = screen_center[i];
+    std::copy(sigma.m.begin(), sigma.m.end(), p.sigma);
+    p.sort_depth = sort_depth;
+    std::copy(h.m.begin(), h.m.end(), p.h);
+    std::copy(h_inv.m.begin(), h_inv.m.end(), p.h_inv);
+    std::copy(footprint_inv.m.begin(), footprint_inv.m.end(), p.footprint_inv);
+    for (int i = 0; i < 3; ++i) p.normal_vis[i] = normal_vis[i];
+    return p;
+  }
+};
+
+struct TileGrid {  // raster.hpp:32-40
+  int tile_size = 16;
+  int tiles_x = 0, tiles_y = 0;
+  std::vector<std::vector<int>> tiles;  // projected indices, ascending (depth, source)
+  uint64_t rn_total = 0;
+  double rn_per_tile = 0;
+  int tile_count() const { return tiles_x * tiles_y; }
+};
+
+struct PixelContribution {  // raster.hpp:69-74
+  int proj;  // index into RenderCache::projected
+  double alpha;
+  double u, v;
+};
+
+struct RenderCache {  // raster.hpp:76-82, filled by render / render_into on the GPU (psm_render_cache)
+  std::vector<ProjectedSurfel> projected;
+  TileGrid grid;
+  std::vector<std::vector<PixelContribution>> pixels;  // per pixel, blend order
+  RasterConfig cfg;
+  int width = 0, height = 0;
+};
+
+struct AlphaSample {  // raster.hpp:103-108
+  double alpha = 0;
+  double u = 0, v = 0;
+  double w2 = 0;
+  bool inside = false;
+};
+
+struct WeightKey {  // raster.hpp:120-124
+  double weight;
+  int proj;
+  int index;
+};
 
 struct BenchRow {  // raster.hpp:150-160
   std::string name;
@@ -330,7 +408,6 @@ inline void reset_plane(Plane<T>& p, int w, int h, int c) {  // raster.cpp:255-2
 // render_into (raster.cpp:273-511) on the GPU; outputs converted to the reference's double planes.
 inline void render_into(RenderTargets& out, const SceneMap& scene, const MatX* labels, const Camera& cam,
                         const RasterConfig& cfg, RenderCache* cache = nullptr) {
-  if (cache) throw std::runtime_error("psimap::b200: RenderCache (backward) is not supported on the GPU path");
   psm_ctx* ctx = b200::context();
   auto up = b200::upload(scene, labels, ctx);
   const int w = cam.width, h = cam.height, c_sem = scene.c_sem(), n_q = labels ? labels->rows() : 0;
@@ -342,7 +419,40 @@ inline void render_into(RenderTargets& out, const SceneMap& scene, const MatX* l
   const psm_camera cc = cam.to_c();
   const psm_raster_config rc = cfg.to_c();
   psm_counters counters{};
-  b200::check(psm_render(ctx, up->sc, &cc, &rc, &tg, &counters), ctx);
+  if (!cache) {
+    b200::check(psm_render(ctx, up->sc, &cc, &rc, &tg, &counters), ctx);
+  } else {  // RenderCache (raster.cpp:310-315,399-403,507-510): sizes first, then the arrays
+    psm_render_cache_out co{};
+    b200::check(psm_render_cache(ctx, up->sc, &cc, &rc, &tg, &counters, &co), ctx);
+    const int tiles_x = (w + cfg.tile_size - 1) / cfg.tile_size, tiles_y = (h + cfg.tile_size - 1) / cfg.tile_size;
+    std::vector<psm_projected> proj(static_cast<size_t>(co.n_projected));
+    std::vector<int32_t> counts(static_cast<size_t>(tiles_x) * tiles_y), lists(static_cast<size_t>(co.n_tile_entries));
+    std::vector<int64_t> offs(npx + 1);
+    std::vector<psm_contribution> con(static_cast<size_t>(co.n_contribs));
+    co.projected = proj.data(); co.projected_cap = co.n_projected;
+    co.tile_counts = counts.data(); co.tile_lists = lists.data(); co.tile_lists_cap = co.n_tile_entries;
+    co.pixel_offsets = offs.data(); co.contribs = con.data(); co.contribs_cap = co.n_contribs;
+    b200::check(psm_render_cache(ctx, up->sc, &cc, &rc, &tg, &counters, &co), ctx);
+    cache->cfg = cfg;
+    cache->width = w;
+    cache->height = h;
+    cache->projected.clear();
+    for (const psm_projected& p : proj) cache->projected.push_back(ProjectedSurfel::from_c(p));
+    cache->grid = TileGrid{};
+    cache->grid.tile_size = cfg.tile_size;
+    cache->grid.tiles_x = tiles_x;
+    cache->grid.tiles_y = tiles_y;
+    cache->grid.rn_total = counters.rn_total;
+    cache->grid.rn_per_tile = counters.rn_per_tile;
+    cache->grid.tiles.assign(counts.size(), {});
+    size_t at = 0;
+    for (size_t t = 0; t < counts.size(); ++t)
+      for (int32_t k = 0; k < counts[t]; ++k) cache->grid.tiles[t].push_back(lists[at++]);
+    cache->pixels.assign(npx, {});
+    for (size_t px = 0; px < npx; ++px)
+      for (int64_t e = offs[px]; e < offs[px + 1]; ++e)
+        cache->pixels[px].push_back({con[e].proj, con[e].alpha, con[e].u, con[e].v});
+  }
   b200::reset_plane(out.color, w, h, 3);
   b200::reset_plane(out.depth, w, h, 2);
   b200::reset_plane(out.normal, w, h, 3);
@@ -367,6 +477,119 @@ inline RenderTargets render(const SceneMap& scene, const MatX* labels, const Cam
   RenderTargets out;
   render_into(out, scene, labels, cam, cfg, cache);
   return out;
+}
+
+// ---- stage functions (raster.hpp:87-126), device-backed (include/psm.h "Stage entry points")
+
+// project_surfel (raster.cpp:94-142): nullopt when culled; throws std::invalid_argument on a
+// degenerate quaternion of a surfel inside the depth range.
+inline std::optional<ProjectedSurfel> project_surfel(const Surfel& s, const Camera& cam, const RasterConfig& cfg) {
+  psm_ctx* ctx = b200::context();
+  double g[13];
+  for (int k = 0; k < 3; ++k) g[k] = s.center[k];
+  for (int k = 0; k < 4; ++k) g[3 + k] = s.rotation[k];
+  g[7] = s.scales[0]; g[8] = s.scales[1]; g[9] = s.opacity;
+  for (int k = 0; k < 3; ++k) g[10 + k] = s.color[k];
+  const psm_camera cc = cam.to_c();
+  const psm_raster_config rc = cfg.to_c();
+  psm_projected p{};
+  int32_t status = 0;
+  b200::check(psm_project_surfels(ctx, g, 1, &cc, &rc, &p, &status, nullptr), ctx);
+  if (!status) return std::nullopt;
+  return ProjectedSurfel::from_c(p);
+}
+
+namespace b200 {
+inline TileGrid bin(const std::vector<ProjectedSurfel>& projected, const Camera& cam, const RasterConfig& cfg,
+                    int binning, double chi2) {
+  psm_ctx* ctx = context();
+  std::vector<psm_projected> pc;
+  pc.reserve(projected.size());
+  for (const auto& p : projected) pc.push_back(p.to_c());
+  TileGrid g;
+  g.tile_size = cfg.tile_size;
+  g.tiles_x = (cam.width + cfg.tile_size - 1) / cfg.tile_size;
+  g.tiles_y = (cam.height + cfg.tile_size - 1) / cfg.tile_size;
+  std::vector<int32_t> counts(static_cast<size_t>(g.tiles_x) * g.tiles_y);
+  const psm_camera cc = cam.to_c();
+  const psm_raster_config rc = cfg.to_c();
+  psm_counters c{};
+  const int64_t n = static_cast<int64_t>(pc.size());
+  check(psm_bin_projected(ctx, pc.data(), n, &cc, &rc, binning, chi2, counts.data(), nullptr, 0, &c), ctx);
+  std::vector<int32_t> lists(static_cast<size_t>(c.rn_total));
+  if (c.rn_total)
+    check(psm_bin_projected(ctx, pc.data(), n, &cc, &rc, binning, chi2, counts.data(), lists.data(),
+                            static_cast<int64_t>(c.rn_total), &c), ctx);
+  g.tiles.assign(counts.size(), {});
+  size_t at = 0;
+  for (size_t t = 0; t < counts.size(); ++t)
+    for (int32_t k = 0; k < counts[t]; ++k) g.tiles[t].push_back(lists[at++]);
+  g.rn_total = c.rn_total;
+  g.rn_per_tile = c.rn_per_tile;
+  return g;
+}
+}  // namespace b200
+
+// bin_circle / bin_aabb (raster.cpp:51-90,144-152)
+inline TileGrid bin_circle(const std::vector<ProjectedSurfel>& projected, const Camera& cam, const RasterConfig& cfg) {
+  return b200::bin(projected, cam, cfg, PSM_BIN_CIRCLE, cfg.chi2);
+}
+inline TileGrid bin_aabb(const std::vector<ProjectedSurfel>& projected, const Camera& cam, const RasterConfig& cfg,
+                         double chi2) {
+  return b200::bin(projected, cam, cfg, PSM_BIN_AABB, chi2);
+}
+
+// sample_surfel_alpha / evaluate_alpha (raster.cpp:154-177)
+inline AlphaSample sample_surfel_alpha(const ProjectedSurfel& proj, const Camera& cam, double px, double py,
+                                       const RasterConfig& cfg) {
+  psm_ctx* ctx = b200::context();
+  const psm_projected p = proj.to_c();
+  const double op = 0.0;
+  const int32_t idx = 0;
+  const psm_camera cc = cam.to_c();
+  const psm_raster_config rc = cfg.to_c();
+  psm_alpha_sample o{};
+  b200::check(psm_sample_alpha(ctx, &p, &op, 1, &idx, &px, &py, 1, &cc, &rc, &o), ctx);
+  AlphaSample a;
+  a.u = o.u; a.v = o.v; a.w2 = o.w2; a.inside = o.inside != 0;  // .alpha stays 0, as the reference leaves it
+  return a;
+}
+inline double evaluate_alpha(const ProjectedSurfel& proj, const Surfel& s, const Camera& cam, double px, double py,
+                             const RasterConfig& cfg) {
+  psm_ctx* ctx = b200::context();
+  const psm_projected p = proj.to_c();
+  const double op = s.opacity;
+  const int32_t idx = 0;
+  const psm_camera cc = cam.to_c();
+  const psm_raster_config rc = cfg.to_c();
+  psm_alpha_sample o{};
+  b200::check(psm_sample_alpha(ctx, &p, &op, 1, &idx, &px, &py, 1, &cc, &rc, &o), ctx);
+  return o.alpha;
+}
+
+// topk_select (raster.cpp:225-251); best_scratch receives the winners in (weight desc, proj asc) order
+inline void topk_select(const WeightKey* keys, int m, int k, std::vector<WeightKey>& best_scratch,
+                        std::vector<char>& selected) {
+  psm_ctx* ctx = b200::context();
+  std::vector<double> w(m);
+  std::vector<int32_t> pj(m);
+  for (int i = 0; i < m; ++i) {
+    w[i] = keys[i].weight;
+    pj[i] = keys[i].proj;
+  }
+  const int64_t offs[2] = {0, m};
+  std::vector<int8_t> sel(m > 0 ? m : 1);
+  b200::check(psm_topk_select(ctx, w.data(), pj.data(), offs, 1, k, sel.data()), ctx);
+  selected.assign(m, 0);
+  best_scratch.clear();
+  for (int i = 0; i < m; ++i)
+    if (sel[i]) {
+      selected[i] = 1;
+      best_scratch.push_back(keys[i]);
+    }
+  std::sort(best_scratch.begin(), best_scratch.end(), [](const WeightKey& a, const WeightKey& b) {
+    return a.weight != b.weight ? a.weight > b.weight : a.proj < b.proj;
+  });
 }
 
 // bench_render (raster.cpp:513-573): the 4-row grid; the scene is uploaded once and
@@ -425,7 +648,7 @@ struct StreetSpec {  // synthetic.hpp (make_street_scene parameters)
   uint64_t seed = 7;
   double min_aspect = 5.0;
   int image_w = 256, image_h = 192;
-  int c_sem = 16;
+  int c_sem = 32;
   int n_instances = 256;
   double scale_mult = 1.0;  // extension: s1 multiplier (1 = the reference's scales)
 };

@@ -274,6 +274,91 @@ typedef struct psm_scene_grads { /* host outputs, each may be NULL */
 int psm_render_backward(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam,
                         const psm_raster_config* cfg, const psm_plane_grads* grads, psm_scene_grads* out);
 
+/* ---- Stage entry points (raster.hpp:87-126) --------------------------------
+ * The reference's stage functions as device-backed batch calls with host inputs and
+ * outputs (synchronous on the context stream). Results are bit-identical to the
+ * reference's: the same fp64 arithmetic as the render pipeline (--fmad=false, the
+ * glibc-exact exp). */
+
+/* ProjectedSurfel (raster.hpp:21-30). 2x2 / 3x3 matrices column-major like Eigen. */
+typedef struct psm_projected {
+  int32_t source;           /* index into the scene (the reference's project_surfel leaves -1) */
+  int32_t pad;
+  double screen_center[2];
+  double sigma[4];          /* J Sigma J^T, pixel^2 */
+  double sort_depth;        /* camera-space z of the centre */
+  double h[9];              /* tangent (u, v, 1) -> camera point */
+  double h_inv[9];
+  double footprint_inv[4];  /* inverse of sigma + 0.3 I */
+  double normal_vis[3];
+} psm_projected;
+
+/* project_surfel (raster.cpp:94-142) of n surfels (N x 13 host AoS). status[i] = 1 when
+ * surfel i projects (out[i] filled, out[i].source = -1 as the reference returns it), 0 when
+ * culled. A degenerate quaternion on a surfel that passes the depth cull returns PSM_EINVAL
+ * (std::invalid_argument in the reference); *bad_index (may be NULL) is its index. */
+int psm_project_surfels(psm_ctx* ctx, const double* surfels13, int64_t n, const psm_camera* cam,
+                        const psm_raster_config* cfg, psm_projected* out, int32_t* status, int64_t* bad_index);
+
+/* bin_circle / bin_aabb (raster.cpp:51-90,144-152) of n projected surfels: per tile (row-major
+ * tiles_x x tiles_y) the indices into `projected` whose box touches it, ordered by
+ * (sort_depth, source). binning: PSM_BIN_CIRCLE (circle box, cfg->chi2) or PSM_BIN_AABB
+ * (aabb box from `chi2`, bin_aabb's argument). tile_counts[tiles] and counters (rn_total,
+ * rn_per_tile, tiles_x/y, nonempty_tiles) are always written; list (cap entries, the
+ * concatenated per-tile lists) when non-NULL and cap >= rn_total. */
+int psm_bin_projected(psm_ctx* ctx, const psm_projected* projected, int64_t n, const psm_camera* cam,
+                      const psm_raster_config* cfg, int32_t binning, double chi2, int32_t* tile_counts,
+                      int32_t* list, int64_t cap, psm_counters* counters);
+
+/* sample_surfel_alpha + evaluate_alpha (raster.cpp:154-177) at m queries: surfel proj_index[q]
+ * of `projected` (opacity[proj_index[q]]) at pixel position (px[q], py[q]). alpha is
+ * evaluate_alpha's (0 outside the support or below alpha_min); u, v, w2, inside are
+ * sample_surfel_alpha's (zero unless inside). */
+typedef struct psm_alpha_sample {
+  double alpha, u, v, w2;
+  int32_t inside;
+  int32_t pad;
+} psm_alpha_sample;
+int psm_sample_alpha(psm_ctx* ctx, const psm_projected* projected, const double* opacity, int64_t n_projected,
+                     const int32_t* proj_index, const double* px, const double* py, int64_t m,
+                     const psm_camera* cam, const psm_raster_config* cfg, psm_alpha_sample* out);
+
+/* topk_select (raster.cpp:225-251) over n_lists independent lists (CSR: list l is entries
+ * [offsets[l], offsets[l+1]) of weights / proj): selected[e] = 1 for the k best entries of
+ * each list by (weight desc, proj asc), all of them when k >= the list's length. k >= 1
+ * (render calls it with max(top_k, 1), raster.cpp:318; k = 0 is undefined in the reference). */
+int psm_topk_select(psm_ctx* ctx, const double* weights, const int32_t* proj, const int64_t* offsets,
+                    int32_t n_lists, int32_t k, int8_t* selected);
+
+/* render with a RenderCache (raster.hpp:75-82, raster.cpp:310-315,399-403,507-510): the render
+ * of psm_render into `targets` (host or device planes) plus the forward intermediates the
+ * reference keeps for the backward pass, as host arrays:
+ *   projected   [n_proj]   the projected surfels in source order (RenderCache::projected)
+ *   tile_counts [tiles]    + tile_lists [rn_total]: TileGrid::tiles as indices into projected
+ *   pixel_offsets [W*H+1]  + contribs [total]: RenderCache::pixels, each pixel's contributors
+ *                          in blend order as (index into projected, alpha, u, v)
+ * Pass NULL arrays (or too-small capacities) to size them: the counts are always returned. */
+typedef struct psm_contribution {
+  int32_t proj;
+  int32_t pad;
+  double alpha, u, v;
+} psm_contribution;
+typedef struct psm_render_cache_out {
+  psm_projected* projected;
+  int64_t projected_cap;
+  int64_t n_projected;     /* out */
+  int32_t* tile_counts;    /* tiles_x * tiles_y entries (NULL: skipped) */
+  int32_t* tile_lists;
+  int64_t tile_lists_cap;
+  int64_t n_tile_entries;  /* out: rn_total */
+  int64_t* pixel_offsets;  /* W*H+1 entries (NULL: skipped) */
+  psm_contribution* contribs;
+  int64_t contribs_cap;
+  int64_t n_contribs;      /* out */
+} psm_render_cache_out;
+int psm_render_cache(psm_ctx* ctx, const psm_scene* scene, const psm_camera* cam, const psm_raster_config* cfg,
+                     const psm_targets* targets, psm_counters* counters, psm_render_cache_out* cache);
+
 /* Workload: make_street_scene (proj/src/synthetic.cpp:236-312) with the same
  * RNG draw order, plus `scale_mult` applied to s1 after it is drawn
  * (density-normalised variants; 1.0 = verbatim). Two-phase:

@@ -87,11 +87,35 @@ class psm_scene_grads(C.Structure):
                 ("center", C.c_void_p), ("rotation", C.c_void_p), ("scales", C.c_void_p)]
 
 
+class psm_projected(C.Structure):  # ProjectedSurfel (raster.hpp:21-30); matrices column-major
+    _fields_ = [("source", C.c_int32), ("pad", C.c_int32), ("screen_center", C.c_double * 2),
+                ("sigma", C.c_double * 4), ("sort_depth", C.c_double), ("h", C.c_double * 9),
+                ("h_inv", C.c_double * 9), ("footprint_inv", C.c_double * 4), ("normal_vis", C.c_double * 3)]
+
+
+class psm_alpha_sample(C.Structure):  # AlphaSample (raster.hpp:103-108) + evaluate_alpha's alpha
+    _fields_ = [("alpha", C.c_double), ("u", C.c_double), ("v", C.c_double), ("w2", C.c_double),
+                ("inside", C.c_int32), ("pad", C.c_int32)]
+
+
+class psm_contribution(C.Structure):  # PixelContribution (raster.hpp:69-74)
+    _fields_ = [("proj", C.c_int32), ("pad", C.c_int32), ("alpha", C.c_double), ("u", C.c_double),
+                ("v", C.c_double)]
+
+
+class psm_render_cache_out(C.Structure):
+    _fields_ = [("projected", C.c_void_p), ("projected_cap", C.c_int64), ("n_projected", C.c_int64),
+                ("tile_counts", C.c_void_p), ("tile_lists", C.c_void_p), ("tile_lists_cap", C.c_int64),
+                ("n_tile_entries", C.c_int64), ("pixel_offsets", C.c_void_p), ("contribs", C.c_void_p),
+                ("contribs_cap", C.c_int64), ("n_contribs", C.c_int64)]
+
+
 # Every symbol include/psm.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED_SYMBOLS = (
     "psm_default_config", "psm_create", "psm_destroy", "psm_last_error", "psm_set_profiling", "psm_get_stage_times",
     "psm_sync", "psm_scene_upload", "psm_scene_free", "psm_scene_info", "psm_render", "psm_render_debug",
     "psm_render_batch", "psm_last_counters", "psm_make_street_scene", "psm_camera_look_at", "psm_camera_make",
     "psm_scene_create", "psm_assign_labels", "psm_render_panoptic", "psm_make_street_scene_ins",
-    "psm_render_backward",
+    "psm_render_backward", "psm_project_surfels", "psm_bin_projected", "psm_sample_alpha", "psm_topk_select",
+    "psm_render_cache",
 )

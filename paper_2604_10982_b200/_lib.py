@@ -48,6 +48,15 @@ def load():
         "psm_render_batch": (C.c_int, [vp, vp, P(A.psm_camera), C.c_int32, P(A.psm_raster_config),
                                        P(A.psm_targets), P(A.psm_counters)]),
         "psm_last_counters": (C.c_int, [vp, P(A.psm_counters)]),
+        "psm_project_surfels": (C.c_int, [vp, vp, C.c_int64, P(A.psm_camera), P(A.psm_raster_config), vp, vp,
+                                          P(C.c_int64)]),
+        "psm_bin_projected": (C.c_int, [vp, vp, C.c_int64, P(A.psm_camera), P(A.psm_raster_config), C.c_int32,
+                                        C.c_double, vp, vp, C.c_int64, P(A.psm_counters)]),
+        "psm_sample_alpha": (C.c_int, [vp, vp, vp, C.c_int64, vp, vp, vp, C.c_int64, P(A.psm_camera),
+                                       P(A.psm_raster_config), vp]),
+        "psm_topk_select": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp]),
+        "psm_render_cache": (C.c_int, [vp, vp, P(A.psm_camera), P(A.psm_raster_config), P(A.psm_targets),
+                                       P(A.psm_counters), P(A.psm_render_cache_out)]),
         "psm_make_street_scene": (C.c_int, [P(A.psm_street_spec), P(C.c_int64), vp, vp, vp, P(A.psm_camera)]),
         "psm_camera_look_at": (C.c_int, [P(C.c_double * 3), P(C.c_double * 3), P(C.c_double * 3), C.c_double,
                                          C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_double,

@@ -23,84 +23,7 @@
 #include "psm_kernels.h"
 #include "psm_panoptic.h"
 
-struct psm_scene {
-  int device = 0;
-  int64_t n = 0;
-  int32_t c_sem = 0, n_q = 0;
-  double* surfels = nullptr;  // N x 13 fp64
-  float* feat = nullptr;      // N x (c_sem + n_q) fp32
-  double* feat64 = nullptr;   // N x (c_sem + n_q) fp64 (PSM_SCENE_EXACT_FEATURES)
-  double* f_ins = nullptr;    // N x c_ins fp64 (assign_labels)
-  int32_t c_ins = 0;
-  int32_t flags = 0;
-};
-
-namespace psm {
-
-struct Buf {
-  void* p = nullptr;
-  size_t bytes = 0;
-};
-
-struct Planes {
-  float *color, *depth, *normal, *sem, *ins, *alpha;
-  int32_t *arg, *cnt;
-  // render_panoptic (pan_ids != NULL): the three id planes and the device query classes
-  int32_t *pan_ids = nullptr, *pan_classes = nullptr, *pan_sem = nullptr;
-  const int32_t* qclass = nullptr;
-  int32_t n_qclass = 0;
-  bool cache = false;  // backward cache: per-pixel contributor lists with transmittance
-};
-
-}  // namespace psm
-
-struct psm_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  cudaStream_t side = nullptr, side2 = nullptr;  // concurrent side work within a frame (large tile buckets)
-  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
-  cudaStream_t copy = nullptr;   // device-to-host copies of finished row bands (host targets)
-  cudaEvent_t band_ev[8] = {};
-  cudaEvent_t copy_done = nullptr;
-  std::string err;
-  bool profiling = false;
-  cudaEvent_t ev[8] = {};
-  int ev_next = 0;
-  psm_stage_times times{};
-  psm_counters last{};
-  // scratch
-  psm::Buf recs, bins, depth_bits, dminmax, tile_counts, cursor, tile_totals, tile_start, kscratch, kscratch2, valid, pos, keys_c, src_c, keys_s, src_s;
-  psm::Buf tkeys, tvals, tkeys2, tvals2, ranges, scan_tmp, hist, khist, totals, dev_small, lists, rank_of, dbg_keys, topk_dbg;
-  psm::Buf lists_w, pan_ids, pan_classes, pan_sem, qclass, lab_tmp, lab_scratch, lab_dist, lab_arg;
-  psm::Buf lists_t, topk_pos, bw_gin, bw_out, tmasks, tclasses;
-  int64_t key_cap = 0;   // tile-key capacity (grow-only, from RN-Total)
-  int32_t list_cap = 0;  // Full-mode per-pixel list capacity (grow-only)
-  psm::Buf plane_color, plane_depth, plane_normal, plane_sem, plane_ins, plane_arg, plane_alpha, plane_cnt;
-  // Pinned counter read-back: one 8-slot record per pending asynchronous frame plus one
-  // for synchronous frames (h_ring[kMaxPend]); h_small points at the current frame's.
-  static constexpr int kMaxPend = 64;
-  int64_t* h_ring = nullptr;
-  int64_t* h_small = nullptr;
-  // Asynchronous frames (device targets, no counters) not yet validated: psm_sync checks
-  // each one's counters in order and, from the first that outgrew its buffers, re-renders
-  // it and every later one (so planes shared between pending frames end as the last wrote
-  // them). A synchronous frame, or a full list, drains the list first.
-  struct Pending {
-    const psm_scene* scene;
-    psm_camera cam;
-    psm_raster_config cfg;
-    psm::Planes pl;
-  };
-  std::vector<Pending> pend;
-  // psm_render_batch: a second context (own stream and scratch) that renders every other
-  // view, so one view's front end overlaps the other's blend and the small latency-bound
-  // launches interleave; created on first use, joined back into `stream` after the batch.
-  psm_ctx* twin = nullptr;
-  cudaEvent_t batch_fork = nullptr, batch_join = nullptr;
-  bool twin_pending = false;  // the twin rendered views not yet validated (psm_sync drains it)
-  bool twin_last = false;     // ... including the batch's last view (its counters are the last)
-};
+#include "psm_ctx.h"
 
 namespace psm {
 namespace {
@@ -140,11 +63,6 @@ int ensure(psm_ctx* ctx, Buf& b, size_t count, T** out) {
   return PSM_OK;
 }
 
-#define PSM_TRY(expr)            \
-  do {                           \
-    int _st = (expr);            \
-    if (_st != PSM_OK) return _st; \
-  } while (0)
 
 void free_buf(Buf& b) {
   if (b.p) cudaFree(b.p);
@@ -940,6 +858,46 @@ int psm_assign_labels(psm_ctx* ctx, psm_scene* sc, const psm_queries* qs, double
   return PSM_OK;
 }
 
+}  // extern "C"
+
+namespace psm {
+
+// The forward in cache mode (RenderCache, raster.cpp:310-315,399-403): planes in context
+// scratch; every pixel's contributors (tile-list position, transmittance before it) in the
+// context's lists; re-rendered until its buffers fit. Synchronous.
+int cache_forward(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg, Planes& pl) {
+  cudaStream_t st = ctx->stream;
+  const size_t npx = static_cast<size_t>(cam->width) * cam->height;
+  pl = Planes{};
+  PSM_TRY(ensure(ctx, ctx->plane_color, npx * 3, &pl.color));
+  PSM_TRY(ensure(ctx, ctx->plane_depth, npx * 2, &pl.depth));
+  PSM_TRY(ensure(ctx, ctx->plane_normal, npx * 3, &pl.normal));
+  PSM_TRY(ensure(ctx, ctx->plane_alpha, npx, &pl.alpha));
+  PSM_TRY(ensure(ctx, ctx->plane_arg, npx, &pl.arg));
+  PSM_TRY(ensure(ctx, ctx->plane_cnt, npx, &pl.cnt));
+  pl.sem = nullptr;
+  pl.ins = nullptr;
+  pl.cache = true;
+  if (ctx->list_cap == 0) ctx->list_cap = 128;
+  PSM_TRY(drain_twin(ctx));  // validate earlier asynchronous frames first
+  if (!ctx->pend.empty()) PSM_TRY(sync_impl(ctx));
+  ctx->h_small = ctx->h_ring + 8 * psm_ctx::kMaxPend;
+  for (int attempt = 0;; ++attempt) {
+    PSM_TRY(render_impl(ctx, sc, cam, cfg, pl, nullptr));
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+    bool rerun = false;
+    PSM_TRY(check_frame(ctx, &rerun));
+    if (!rerun) break;
+    if (attempt >= 3) return fail(ctx, PSM_ENOMEM, "render buffers did not converge");
+  }
+  finish_counters(ctx);
+  return PSM_OK;
+}
+
+}  // namespace psm
+
+extern "C" {
+
 int psm_render_backward(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
                         const psm_plane_grads* g, psm_scene_grads* out) {
   if (!ctx || !sc || !cam || !cfg || !g || !out) return PSM_EINVAL;
@@ -950,29 +908,8 @@ int psm_render_backward(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam
   const int64_t n = sc->n;
   const int cs = sc->c_sem, nq = sc->n_q, W = cam->width, H = cam->height;
   const size_t npx = static_cast<size_t>(W) * H;
-  // forward in cache mode (planes in context scratch), re-rendered until its buffers fit
   psm::Planes pl{};
-  PSM_TRY(psm::ensure(ctx, ctx->plane_color, npx * 3, &pl.color));
-  PSM_TRY(psm::ensure(ctx, ctx->plane_depth, npx * 2, &pl.depth));
-  PSM_TRY(psm::ensure(ctx, ctx->plane_normal, npx * 3, &pl.normal));
-  PSM_TRY(psm::ensure(ctx, ctx->plane_alpha, npx, &pl.alpha));
-  PSM_TRY(psm::ensure(ctx, ctx->plane_arg, npx, &pl.arg));
-  PSM_TRY(psm::ensure(ctx, ctx->plane_cnt, npx, &pl.cnt));
-  pl.sem = nullptr;
-  pl.ins = nullptr;
-  pl.cache = true;
-  if (ctx->list_cap == 0) ctx->list_cap = 128;
-  PSM_TRY(psm::drain_twin(ctx));  // validate earlier asynchronous frames first
-  if (!ctx->pend.empty()) PSM_TRY(psm::sync_impl(ctx));
-  ctx->h_small = ctx->h_ring + 8 * psm_ctx::kMaxPend;
-  for (int attempt = 0;; ++attempt) {
-    PSM_TRY(psm::render_impl(ctx, sc, cam, cfg, pl, nullptr));
-    PSM_CUDA_TRY(cudaStreamSynchronize(st));
-    bool rerun = false;
-    PSM_TRY(psm::check_frame(ctx, &rerun));
-    if (!rerun) break;
-    if (attempt >= 3) return psm::fail(ctx, PSM_ENOMEM, "render buffers did not converge");
-  }
+  PSM_TRY(psm::cache_forward(ctx, sc, cam, cfg, pl));
   psm::finish_counters(ctx);
   // upstream plane gradients to the device
   const size_t n_gc = g->color ? npx * 3 : 0, n_gs = (g->sem_feat && cs > 0) ? npx * cs : 0,
@@ -1039,6 +976,119 @@ int psm_render_backward(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam
   PSM_TRY(d2h(out->rotation, o_r, 4 * nn));
   PSM_TRY(d2h(out->scales, o_s, 2 * nn));
   PSM_CUDA_TRY(cudaStreamSynchronize(st));
+  return PSM_OK;
+}
+
+int psm_render_cache(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const psm_raster_config* cfg,
+                     const psm_targets* targets, psm_counters* counters, psm_render_cache_out* cache) {
+  if (!ctx || !sc || !cam || !cfg || !targets) return PSM_EINVAL;
+  // 1. the render itself into the caller's targets (synchronous: counters requested)
+  psm_counters c{};
+  PSM_TRY(psm::render_common(ctx, sc, cam, cfg, targets, &c, nullptr));
+  if (counters) *counters = c;
+  if (!cache) return PSM_OK;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = sc->n;
+  const int W = cam->width, H = cam->height;
+  const int64_t npx = static_cast<int64_t>(W) * H;
+  // 2. the forward in cache mode: contributor lists in context scratch
+  psm::Planes pl{};
+  PSM_TRY(psm::cache_forward(ctx, sc, cam, cfg, pl));
+  const int tiles = ctx->last.tiles_x * ctx->last.tiles_y;
+  const int64_t rn = static_cast<int64_t>(ctx->last.rn_total);
+  // 3. projected index of every source: exclusive scan of the projection flags
+  uint32_t *proj_of = nullptr, *scan_tmp = nullptr, *n_proj_dev = nullptr;
+  int64_t* offs = nullptr;
+  uint32_t* scan_tmp2 = nullptr;
+  uint32_t* tot = nullptr;
+  PSM_TRY(psm::ensure(ctx, ctx->pos, n > 0 ? n : 1, &proj_of));
+  PSM_TRY(psm::ensure(ctx, ctx->scan_tmp, psm::scan_cta_words(n > npx ? n : npx) + 8, &scan_tmp));
+  PSM_TRY(psm::ensure(ctx, ctx->totals, 512, &tot));
+  n_proj_dev = tot + 256;
+  uint32_t n_proj = 0;
+  if (n > 0) {
+    psm::exclusive_scan_i32(static_cast<const int32_t*>(ctx->valid.p), n, proj_of, n_proj_dev, scan_tmp, st);
+    PSM_CUDA_TRY(cudaGetLastError());
+    PSM_CUDA_TRY(cudaMemcpyAsync(&n_proj, n_proj_dev, sizeof n_proj, cudaMemcpyDeviceToHost, st));
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  cache->n_projected = n_proj;
+  cache->n_tile_entries = rn;
+  // per-pixel offsets: exclusive scan of the contributor counts (<= list_cap after cache_forward)
+  uint32_t* off32 = nullptr;
+  PSM_TRY(psm::ensure(ctx, ctx->keys_c, npx + 1, reinterpret_cast<uint64_t**>(&offs)));
+  PSM_TRY(psm::ensure(ctx, ctx->src_c, npx + 1, &off32));
+  scan_tmp2 = tot + 300;
+  uint32_t total = 0;
+  if (npx > 0) {
+    psm::exclusive_scan_i32(pl.cnt, npx, off32, scan_tmp2, scan_tmp, st);
+    PSM_CUDA_TRY(cudaGetLastError());
+    PSM_CUDA_TRY(cudaMemcpyAsync(&total, scan_tmp2, sizeof total, cudaMemcpyDeviceToHost, st));
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  cache->n_contribs = total;
+  std::vector<int64_t> hoffs(static_cast<size_t>(npx) + 1);
+  {
+    std::vector<uint32_t> h32(static_cast<size_t>(npx));
+    if (npx > 0) PSM_CUDA_TRY(cudaMemcpy(h32.data(), off32, sizeof(uint32_t) * npx, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < npx; ++i) hoffs[i] = h32[i];
+    hoffs[npx] = total;
+  }
+  if (cache->pixel_offsets) std::memcpy(cache->pixel_offsets, hoffs.data(), sizeof(int64_t) * (npx + 1));
+  if (cache->contribs && cache->contribs_cap >= static_cast<int64_t>(total) && total > 0) {
+    psm_contribution* dcon = nullptr;
+    PSM_CUDA_TRY(cudaMemcpyAsync(offs, hoffs.data(), sizeof(int64_t) * (npx + 1), cudaMemcpyHostToDevice, st));
+    PSM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dcon), sizeof(psm_contribution) * total, st));
+    psm::launch_cache_pixels(static_cast<const uint2*>(ctx->lists.p), ctx->list_cap, pl.cnt, offs,
+                             static_cast<const uint32_t*>(ctx->tvals.p), static_cast<const psm::SurfRec*>(ctx->recs.p),
+                             proj_of, W, H, cam->cx, cam->cy, cam->fx, cam->fy, dcon, st);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(cache->contribs, dcon, sizeof(psm_contribution) * total, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(dcon, st);
+    if (e != cudaSuccess) return psm::fail_cuda(ctx, e, "cache contributions", __FILE__, __LINE__);
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  // 4. RenderCache::projected (source order) and the tile lists as projected indices
+  if (cache->projected && cache->projected_cap >= static_cast<int64_t>(n_proj) && n_proj > 0) {
+    psm_projected* dproj = nullptr;
+    PSM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dproj), sizeof(psm_projected) * n_proj, st));
+    psm::DevCamera dc;
+    std::memcpy(dc.r, cam->r_cw, sizeof dc.r);
+    std::memcpy(dc.t, cam->t_cw, sizeof dc.t);
+    dc.fx = cam->fx; dc.fy = cam->fy; dc.cx = cam->cx; dc.cy = cam->cy;
+    dc.w = W; dc.h = H; dc.near_clip = cam->near_clip; dc.far_clip = cam->far_clip;
+    psm::launch_cache_projected(sc->surfels, n, dc, cfg->chi2, static_cast<const int32_t*>(ctx->valid.p), proj_of,
+                                dproj, st);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(cache->projected, dproj, sizeof(psm_projected) * n_proj, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(dproj, st);
+    if (e != cudaSuccess) return psm::fail_cuda(ctx, e, "cache projected", __FILE__, __LINE__);
+    PSM_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  if (cache->tile_counts || (cache->tile_lists && cache->tile_lists_cap >= rn)) {
+    std::vector<int32_t> rg(static_cast<size_t>(tiles) * 2);
+    if (tiles > 0)
+      PSM_CUDA_TRY(cudaMemcpy(rg.data(), ctx->ranges.p, sizeof(int32_t) * 2 * tiles, cudaMemcpyDeviceToHost));
+    if (cache->tile_counts)
+      for (int t = 0; t < tiles; ++t) cache->tile_counts[t] = rg[2 * t + 1] - rg[2 * t];
+    if (cache->tile_lists && cache->tile_lists_cap >= rn && rn > 0) {
+      // the tile buckets are dense in tile order over [0, rn_total) (K3's exclusive scan)
+      int32_t* dl = nullptr;
+      PSM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dl), sizeof(int32_t) * rn, st));
+      psm::launch_gather_proj(static_cast<const uint32_t*>(ctx->tvals.p), proj_of, rn, dl, st);
+      std::vector<int32_t> all(static_cast<size_t>(rn));
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaMemcpyAsync(all.data(), dl, sizeof(int32_t) * rn, cudaMemcpyDeviceToHost, st);
+      cudaFreeAsync(dl, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return psm::fail_cuda(ctx, e, "cache tile lists", __FILE__, __LINE__);
+      int64_t at = 0;
+      for (int t = 0; t < tiles; ++t)
+        for (int32_t q = rg[2 * t]; q < rg[2 * t + 1]; ++q) cache->tile_lists[at++] = all[q];
+    }
+  }
   return PSM_OK;
 }
 

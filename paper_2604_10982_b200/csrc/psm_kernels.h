@@ -130,6 +130,14 @@ void radix_sort_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t
                     int64_t cap, int begin_bit, int end_bit, uint32_t* hist, uint32_t* totals, cudaStream_t st,
                     bool* result_in_alt);
 
+// stages.cu: RenderCache outputs (psm_render_cache)
+void launch_cache_pixels(const uint2* lists, int list_cap, const int32_t* cnt, const int64_t* offs,
+                         const uint32_t* vals, const SurfRec* recs, const uint32_t* proj_of, int width, int height,
+                         double cx, double cy, double fx, double fy, psm_contribution* out, cudaStream_t st);
+void launch_cache_projected(const double* s13, int64_t n, const DevCamera& cam, double chi2, const int32_t* valid,
+                            const uint32_t* proj_of, psm_projected* out, cudaStream_t st);
+void launch_gather_proj(const uint32_t* vals, const uint32_t* proj_of, int64_t n, int32_t* out, cudaStream_t st);
+
 // blend.cu
 int blend_kmax_for(int k_sel);
 int blend_nch_for(int feat_dims);
