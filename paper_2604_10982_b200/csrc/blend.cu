@@ -376,7 +376,12 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         mq = max(mq, __shfl_xor_sync(0xffffffffu, mq, o));
         m4 = max(m4, __shfl_xor_sync(0xffffffffu, m4, o));
       }
+      const unsigned cmask = cnt >= 32 ? 0xffffffffu : (1u << cnt) - 1u;
+      const bool none_done = !__any_sync(0xffffffffu, done && inside);
       if (lane == 0) {
+        PSM_STAT(13, __popc(~full & cmask));
+        if (none_done) PSM_STAT(14, __popc(~full & cmask));
+        PSM_STAT(15, none_done ? cnt : 0);
         PSM_STAT(9, __popc(full));
         PSM_STAT(10, kPer * iters);
         PSM_STAT(11, mq);

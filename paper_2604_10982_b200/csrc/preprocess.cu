@@ -80,7 +80,9 @@ __device__ __forceinline__ bool project_one(int64_t i, const double* __restrict_
   bins[i] = b;
   const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(pf.pc2));
   depth_bits[i] = bits;
+#ifndef PSM_PRE_NOCOUNT
   count_tiles(b, pf.cx, pf.cy, rs, cam.h, tile_counts);
+#endif
   valid[i] = 1;
   *db = bits;
   return true;
@@ -97,14 +99,18 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-constexpr int kPreSmem = 2 * 8 * 32 * 13 * static_cast<int>(sizeof(double));  // 53,248 B
+#ifndef PSM_PRE_WARPS
+#define PSM_PRE_WARPS 8
+#endif
+constexpr int kPreWarps = PSM_PRE_WARPS;
+constexpr int kPreSmem = 2 * kPreWarps * 32 * 13 * static_cast<int>(sizeof(double));  // 53,248 B at 8 warps
 
 // 2 CTAs per SM (126 registers, no spills) with the batch prefetch: C3 preprocess 0.130 ->
 // 0.120 ms, C4 0.552 -> 0.505 ms; at 3 CTAs the persistent loop spills (0.150 ms)
 #ifndef PSM_PRE_MINB
 #define PSM_PRE_MINB 2
 #endif
-__global__ void __launch_bounds__(256, PSM_PRE_MINB) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
+__global__ void __launch_bounds__(32 * kPreWarps, PSM_PRE_MINB) preprocess_kernel(const double* __restrict__ surfels13, int64_t n,
                                                           DevCamera cam, DevRaster rs, SurfRec* __restrict__ recs,
                                                           BinRec* __restrict__ bins,
                                                           uint64_t* __restrict__ depth_bits,
@@ -117,13 +123,13 @@ __global__ void __launch_bounds__(256, PSM_PRE_MINB) preprocess_kernel(const dou
   // next batch's copies in flight while this one is projected.
   extern __shared__ __align__(16) double stage[];  // [2][8 warps][32 * 13]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t n_batches = (n + 31) / 32, stride = static_cast<int64_t>(gridDim.x) * 8;
+  const int64_t n_batches = (n + 31) / 32, stride = static_cast<int64_t>(gridDim.x) * kPreWarps;
   auto issue = [&](int64_t bt, int buf) {
     if (bt < n_batches) {
       const int64_t w0 = bt * 32;
       const int nw = static_cast<int>(n - w0 < 32 ? n - w0 : 32);
       const double* src = surfels13 + 13 * w0;
-      double* dst = stage + (buf * 8 + w) * (32 * 13);
+      double* dst = stage + (buf * kPreWarps + w) * (32 * 13);
       const int nv = (13 * nw) / 2;  // whole 16-byte pairs (13 * 32 is even)
 #pragma unroll
       for (int k = 0; k < 7; ++k) {
@@ -137,7 +143,7 @@ __global__ void __launch_bounds__(256, PSM_PRE_MINB) preprocess_kernel(const dou
   unsigned long long lo = ~0ull, hi = 0ull;
   uint32_t n_ok = 0;
   int buf = 0;
-  int64_t bt = static_cast<int64_t>(blockIdx.x) * 8 + w;
+  int64_t bt = static_cast<int64_t>(blockIdx.x) * kPreWarps + w;
   issue(bt, 0);
   for (; bt < n_batches; bt += stride, buf ^= 1) {
     issue(bt + stride, buf ^ 1);
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(256, PSM_PRE_MINB) preprocess_kernel(const dou
     __syncwarp();
     const int64_t i = bt * 32 + lane;
     uint64_t db = 0;
-    const bool ok = i < n && project_one(i, stage + (buf * 8 + w) * (32 * 13) + 13 * lane, cam, rs, recs, bins, depth_bits,
+    const bool ok = i < n && project_one(i, stage + (buf * kPreWarps + w) * (32 * 13) + 13 * lane, cam, rs, recs, bins, depth_bits,
                                          tile_counts, valid, &db, err);
     if (ok) {
       lo = db < lo ? db : lo;
@@ -205,13 +211,13 @@ void launch_preprocess(const double* surfels13, int64_t n, const DevCamera& cam,
   if (!per_sm[dev]) {
     cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(preprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPreSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], preprocess_kernel, 256, kPreSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], preprocess_kernel, 32 * kPreWarps, kPreSmem);
     if (per_sm[dev] < 1) per_sm[dev] = 1;
   }
-  const int64_t need = (n + 255) / 256;
+  const int64_t need = (n + 32 * kPreWarps - 1) / (32 * kPreWarps);
   const int64_t resident = static_cast<int64_t>(per_sm[dev]) * sms[dev];
   const int64_t blocks = need < resident ? need : resident;
-  preprocess_kernel<<<static_cast<unsigned>(blocks), 256, kPreSmem, stream>>>(surfels13, n, cam, rs, recs, bins, depth_bits,
+  preprocess_kernel<<<static_cast<unsigned>(blocks), 32 * kPreWarps, kPreSmem, stream>>>(surfels13, n, cam, rs, recs, bins, depth_bits,
                                                                        tile_counts, valid, n_proj, depth_minmax, err);
 }
 
