@@ -115,10 +115,10 @@ __host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) / 16 * 
 #ifndef PSM_BLEND_TMA
 #define PSM_BLEND_TMA 0
 #endif
-// per warp: [2][chunk] staged records + [2][chunk] their list positions (16 B aligned)
-// + the two buffers' mbarriers
+// per warp: [2][chunk] staged records + [2][chunk] their list positions + [2][chunk] their
+// source ids (16 B aligned) + the two buffers' mbarriers
 __host__ __device__ constexpr size_t warp_stage_bytes(int kmax) {
-  return align16(2 * chunk_for(kmax) * (sizeof(SurfRec) + sizeof(int))) + 16;
+  return align16(2 * chunk_for(kmax) * (sizeof(SurfRec) + 2 * sizeof(int))) + 16;
 }
 __host__ __device__ constexpr size_t stage_bytes(int kmax) {
   return static_cast<size_t>(cta_warps(kmax)) * warp_stage_bytes(kmax);
@@ -137,6 +137,10 @@ static_assert(PSM_BLEND_CH0 <= 32 && PSM_BLEND_CH8 <= 32 && PSM_BLEND_CH16 <= 32
 // Slots hold list positions; the source ids are only looked up on an exact weight tie.
 __device__ __forceinline__ bool before(double wa, int pa, double wb, int pb, const uint32_t* __restrict__ vals) {
   return wa > wb || (wa == wb && __ldg(vals + pa) < __ldg(vals + pb));
+}
+// The same order when the slots hold source ids (the Top-K renders, see kSrcSlots): no loads.
+__device__ __forceinline__ bool before_src(double wa, int sa, double wb, int sb) {
+  return wa > wb || (wa == wb && sa < sb);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -244,6 +248,11 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
 
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
   int* spos = reinterpret_cast<int*>(stage + 2 * kChunk);  // [2][kChunk] list positions of the staged records
+  int* ssrc = spos + 2 * kChunk;                           // [2][kChunk] their source ids
+  // Top-K slots hold source ids (ties compare them directly, the feature phase reads them
+  // as they are) unless list positions are needed later: the backward cache's selected
+  // positions (FULL_LIST) and the panoptic phase's blend-order re-sort (PANO_T).
+  constexpr bool kSrcSlots = !FULL_LIST && PANO_T == 0;
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(stage) + warp_stage_bytes(KMAX) - 16);
   unsigned pending = 0;  // buffers with a bulk-copy phase not yet waited on
   // The tile list is read in 32-entry windows (source id + warp-block mask per lane, the
@@ -289,6 +298,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         for (int k = 0; k < kRecVec; ++k) cp_async16(d + 16 * k, g + 16 * k);
 #endif
         spos[bf * kChunk + filled + r] = wb + lane;
+        if constexpr (kSrcSlots) ssrc[bf * kChunk + filled + r] = static_cast<int>(cv);
       }
       filled += __popc(take);
       clive &= ~take;
@@ -456,18 +466,23 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
           if constexpr (KMAX > 0) {
             // insertion select (raster.cpp:238-249); below the threshold weight (the common
             // case once the list is full) one compare decides
-            if (wt >= thr_w && before(wt, pos, thr_w, thr_p, p.vals)) {
+            auto bef = [&](double wa, int ka, double wb, int kb) {
+              if constexpr (kSrcSlots) return before_src(wa, ka, wb, kb);
+              else return before(wa, ka, wb, kb, p.vals);
+            };
+            if (wt >= thr_w && bef(wt, kSrcSlots ? ssrc[buf * kChunk + j] : pos, thr_w, thr_p)) {
+              const int key = kSrcSlots ? ssrc[buf * kChunk + j] : pos;
               int i = n_top < klen ? n_top++ : klen - 1;  // the list fills without a threshold
               while (i > 0) {
                 const double w = top_w[(i - 1) * kCT + tid];
                 const int q = top_p[(i - 1) * kCT + tid];
-                if (!before(wt, pos, w, q, p.vals)) break;
+                if (!bef(wt, key, w, q)) break;
                 top_w[i * kCT + tid] = w;
                 top_p[i * kCT + tid] = q;
                 --i;
               }
               top_w[i * kCT + tid] = wt;
-              top_p[i * kCT + tid] = pos;
+              top_p[i * kCT + tid] = key;
               if (n_top == klen) {
                 thr_w = top_w[(klen - 1) * kCT + tid];
                 thr_p = top_p[(klen - 1) * kCT + tid];
@@ -535,7 +550,8 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       if (p.topk_dbg) {
         for (int i = 0; i < k_sel; ++i)
           p.topk_dbg[pix * k_sel + i] =
-              i < blend_n ? static_cast<int>(__ldg(p.vals + top_p[i * kCT + tid])) : -1;
+              i < blend_n ? (kSrcSlots ? top_p[i * kCT + tid] : static_cast<int>(__ldg(p.vals + top_p[i * kCT + tid])))
+                          : -1;
       }
     }
     if constexpr (FULL_LIST) {
@@ -571,7 +587,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       // over the slot's weight cell, read back below with one 8-byte load per row
       int2* slot = reinterpret_cast<int2*>(top_w);
       for (int i = 0; i < blend_n; ++i) {
-        const int s = static_cast<int>(__ldg(p.vals + top_p[i * kCT + tid]));
+        const int s = kSrcSlots ? top_p[i * kCT + tid] : static_cast<int>(__ldg(p.vals + top_p[i * kCT + tid]));
         slot[i * kCT + tid] = make_int2(s, __float_as_int(static_cast<float>(top_w[i * kCT + tid])));
       }
       __syncwarp();
