@@ -75,6 +75,56 @@ __global__ void __launch_bounds__(256) assign_labels_kernel(LabelParams p) {
   write_rows(p, s, best);
 }
 
+// Up to 32 alive queries: a warp keeps its 32 surfels' A values / probabilities in shared
+// memory ([query][33] per warp, padded against bank conflicts) instead of the global
+// scratch, and then writes the 32 rows cooperatively: lane = column, so every row store
+// is one coalesced run (the per-thread row stores of the general path touch one 32-byte
+// sector per lane and value).
+constexpr int kRowsMaxAlive = 32;
+constexpr int kRowsWarps = 8;
+__global__ void __launch_bounds__(32 * kRowsWarps) assign_labels_rows_kernel(LabelParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* tab = reinterpret_cast<uint64_t*>(smem);
+  double* vals = reinterpret_cast<double*>(smem + 2048);  // [warp][kRowsMaxAlive][33]
+  double* qs = vals + kRowsWarps * kRowsMaxAlive * 33;
+  stage_tables(p, qs, tab);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* wv = vals + warp * kRowsMaxAlive * 33;
+  const int64_t s0 = (static_cast<int64_t>(blockIdx.x) * kRowsWarps + warp) * 32;
+  const int64_t s = s0 + lane;
+  const double* mean = qs + p.n_alive * p.c_ins;
+  const double* inv = mean + 3 * p.n_alive;
+  int best = -1;
+  if (s < p.n && p.n_alive > 0) {
+    const double center[3] = {p.surfels[s * 13 + 0], p.surfels[s * 13 + 1], p.surfels[s * 13 + 2]};
+    const int b = psm_assign_one(p.f_ins + s * p.c_ins, p.c_ins, center, p.n_alive, qs, mean, inv, wv + lane, 33,
+                                 tab);
+    best = p.alive_index[b];
+  }
+  if (s < p.n && p.argmax) p.argmax[s] = best;
+  __syncwarp();
+  const int D = p.c_sem + p.n_q;
+  const bool carry = p.feat_out != p.feat_in;  // f_sem columns move to new rows
+  for (int j = 0; j < 32; ++j) {
+    const int64_t sj = s0 + j;
+    if (sj >= p.n) break;
+    float* row32 = p.feat_out + sj * D;
+    double* row64 = p.feat64_out ? p.feat64_out + sj * D : nullptr;
+    if (carry)
+      for (int c = lane; c < p.c_sem; c += 32) {
+        row32[c] = p.feat_in[sj * p.d_in + c];
+        if (row64) row64[c] = p.feat64_in[sj * p.d_in + c];
+      }
+    for (int q = lane; q < p.n_q; q += 32) {
+      const int a = p.alive_slot[q];
+      const double v = a >= 0 ? wv[a * 33 + j] : 0.0;
+      row32[p.c_sem + q] = static_cast<float>(v);
+      if (row64) row64[p.c_sem + q] = v;
+      if (p.dist) p.dist[sj * p.n_q + q] = v;
+    }
+  }
+}
+
 }  // namespace
 
 void launch_assign_labels(const LabelParams& p, cudaStream_t st) {
@@ -87,8 +137,20 @@ void launch_assign_labels(const LabelParams& p, cudaStream_t st) {
     cudaFuncSetAttribute(assign_labels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
     configured |= 1ull << dev;
   }
-  const unsigned blocks = static_cast<unsigned>((p.n + 255) / 256);
   const int words = p.n_alive * (p.c_ins + 12);
+  if (p.n_alive <= kRowsMaxAlive && words <= kQsWords) {
+    static unsigned long long configured_rows = 0;
+    const int most = 2048 + static_cast<int>(sizeof(double)) * (kRowsWarps * kRowsMaxAlive * 33 + kQsWords);
+    if (!(configured_rows >> dev & 1ull)) {
+      cudaFuncSetAttribute(assign_labels_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+      configured_rows |= 1ull << dev;
+    }
+    const size_t smem = 2048 + sizeof(double) * (kRowsWarps * kRowsMaxAlive * 33 + words);
+    const unsigned blocks = static_cast<unsigned>((p.n + 32 * kRowsWarps - 1) / (32 * kRowsWarps));
+    assign_labels_rows_kernel<<<blocks, 32 * kRowsWarps, smem, st>>>(p);
+    return;
+  }
+  const unsigned blocks = static_cast<unsigned>((p.n + 255) / 256);
   const size_t smem = 2048 + (words <= kQsWords ? sizeof(double) * words : 0);
   assign_labels_kernel<<<blocks, 256, smem, st>>>(p);
 }
