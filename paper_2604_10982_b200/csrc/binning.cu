@@ -311,10 +311,10 @@ __global__ void __launch_bounds__(32 * kEmitWarps, PSM_EMIT_MINB) emit_kernel(co
       EmitItem& it = items[warp][lane];
       // the key's source field is (source << 8 | block mask), kFieldExtra bits wider than the source
       const int fb = src_bits + kFieldExtra;
-      it.key = sort_key(depth_bits[i], static_cast<uint64_t>(i) << kFieldExtra, depth_minmax[0],
+      it.key = sort_key(b.depth_bits, static_cast<uint64_t>(i) << kFieldExtra, depth_minmax[0],
                         key_shift(depth_minmax, fb), fb);
       if (ellipse || masks_on) {
-        it.e = psm_ellipse_prep(recs[i].cx, recs[i].cy, b.F00, b.F01, b.F11, rs.chi2);
+        it.e = psm_ellipse_prep(b.cx, b.cy, b.F00, b.F01, b.F11, rs.chi2);
       } else {
         it.e.ok = 0;
       }

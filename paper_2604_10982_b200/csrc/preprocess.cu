@@ -76,9 +76,11 @@ __device__ __forceinline__ bool project_one(int64_t i, const double* __restrict_
   b.tx1 = min(x86_cvt(floor(psm_div_tile(x1, ts))), rs.tiles_x - 1);
   b.ty0 = max(x86_cvt(floor(psm_div_tile(y0, ts))), 0);
   b.ty1 = min(x86_cvt(floor(psm_div_tile(y1, ts))), rs.tiles_y - 1);
-  b.pad0 = b.pad1 = 0;
-  bins[i] = b;
   const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(pf.pc2));
+  b.cx = pf.cx;
+  b.cy = pf.cy;
+  b.depth_bits = bits;
+  bins[i] = b;
   depth_bits[i] = bits;
 #ifndef PSM_PRE_NOCOUNT
   count_tiles(b, pf.cx, pf.cy, rs, cam.h, tile_counts);

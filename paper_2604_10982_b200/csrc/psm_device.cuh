@@ -5,8 +5,9 @@
 //                 colour + normal_vis (raster.cpp:324-353), packed so one record
 //                 is nine 16-byte loads and the 5 support-test scalars share the
 //                 first 48 bytes.
-//   BinRec   [N]  48 B: the dilated covariance F (raster.cpp:19-24) and the
-//                 clamped tile rectangle of the active box (raster.cpp:59-68).
+//   BinRec   [N]  64 B: the dilated covariance F (raster.cpp:19-24), the screen
+//                 centre, the depth bits and the clamped tile rectangle of the
+//                 active box (raster.cpp:59-68): everything K4 reads per surfel.
 //   depth    [N]  uint64 bit pattern of sort_depth (positive doubles order as
 //                 unsigned integers, so a radix sort reproduces (depth, source)).
 #ifndef PSM_DEVICE_CUH
@@ -31,10 +32,11 @@ static_assert(sizeof(SurfRec) == 144, "SurfRec must be 144 bytes");
 
 struct __align__(16) BinRec {
   double F00, F01, F11;  // footprint_cov(sigma)
+  double cx, cy;         // screen centre (the emit's ellipse rows and warp-block masks)
+  uint64_t depth_bits;   // sort_depth's bit pattern (the emit's sort key)
   int32_t tx0, tx1, ty0, ty1;  // clamped tile rectangle of the binning box (empty if tx0 > tx1)
-  int32_t pad0, pad1;
 };
-static_assert(sizeof(BinRec) == 48, "BinRec must be 48 bytes");
+static_assert(sizeof(BinRec) == 64, "BinRec must be 64 bytes (one record per emit read)");
 
 // Sub-buckets per tile for the counting sort's atomics (binning.cu).
 constexpr int kSplit = 32;
