@@ -1,6 +1,7 @@
 """ctypes wrapper of oracle/_ref/libpsimap_ref.so: the REFERENCE'S OWN render path
-(/root/reference/proj/src/{raster,math_util,core_types,synthetic}.cpp, compiled unchanged
-by oracle/ref/Makefile against the minimal Eigen stand-in oracle/eigen_min).
+(/root/reference/proj/src/{raster,math_util,core_types,synthetic}.cpp) and panoptic rows
+(panoptic.cpp assign_labels, metrics.cpp render_panoptic), compiled unchanged by
+oracle/ref/Makefile against the minimal Eigen stand-in oracle/eigen_min.
 TEST INFRASTRUCTURE ONLY: imported by tests/ and by bench.py's reference arm, never by
 the product package.
 
@@ -70,6 +71,9 @@ def load():
                                             P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_int32)]),
         "ref_topk_select": (None, [vp, vp, C.c_int32, C.c_int32, vp]),
         "ref_bench_render": (C.c_int, [vp, P(A.psm_camera), C.c_int32, P(A.psm_raster_config), vp]),
+        "ref_assign_labels": (C.c_int, [vp, C.c_int64, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp]),
+        "ref_render_panoptic": (C.c_int, [vp, C.c_int64, vp, C.c_int32, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp,
+                                          P(A.psm_camera), P(A.psm_raster_config), vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -200,3 +204,39 @@ def topk_select(weights, proj, k: int) -> np.ndarray:
     sel = np.zeros(len(w), dtype=np.int8)
     load().ref_topk_select(_p(w), _p(p), len(w), k, _p(sel))
     return sel.astype(bool)
+
+
+def _queries(queries, c_ins):
+    from paper_2604_10982_b200.panoptic import pack_queries
+    return pack_queries(queries, c_ins)
+
+
+def assign_labels(surfels13, f_ins, queries):
+    """assign_labels (panoptic.cpp:36-91) by the reference: (dist (N, Q) per-surfel rows, argmax (N,))."""
+    s = np.ascontiguousarray(np.asarray(surfels13, dtype=np.float64).reshape(-1, 13))
+    n = s.shape[0]
+    f = np.ascontiguousarray(np.asarray(f_ins, dtype=np.float64).reshape(n, -1))
+    feat, mean, cov, alive, _ = _queries(queries, f.shape[1])
+    q = len(queries)
+    dist = np.zeros((n, q))
+    arg = np.zeros(n, np.int32)
+    if load().ref_assign_labels(_p(s), n, _p(f), f.shape[1], q, _p(feat), _p(mean), _p(cov), _p(alive), _p(dist),
+                                _p(arg)) != 0:
+        raise ValueError("assign_labels failed")
+    return dist, arg
+
+
+def render_panoptic(scene, cam, cfg) -> dict:
+    """render_panoptic (metrics.cpp:339-369) by the reference over scene.surfels / f_sem / f_ins / queries."""
+    s = scene.surfels
+    n = s.shape[0]
+    f = np.ascontiguousarray(scene.f_sem)
+    fi = np.ascontiguousarray(scene.f_ins)
+    feat, mean, cov, alive, cls = _queries(scene.queries, fi.shape[1])
+    w, h = cam.width, cam.height
+    out = {k: np.zeros((h, w, 1), np.int32) for k in ("ids", "classes", "sem_classes")}
+    if load().ref_render_panoptic(_p(s), n, _p(f), f.shape[1], _p(fi), fi.shape[1], len(scene.queries), _p(feat),
+                                  _p(mean), _p(cov), _p(alive), _p(cls), C.byref(cam.to_c()), C.byref(cfg.to_c()),
+                                  _p(out["ids"]), _p(out["classes"]), _p(out["sem_classes"])) != 0:
+        raise ValueError("render_panoptic failed")
+    return out

@@ -1,6 +1,7 @@
 // ref_capi.cpp — C-ABI over the REFERENCE'S OWN render path, compiled unchanged from
-// /root/reference/proj/src/{raster,math_util,core_types,synthetic}.cpp against the
-// minimal Eigen stand-in in oracle/eigen_min (see its header for the numerics it keeps).
+// /root/reference/proj/src/{raster,math_util,core_types,synthetic,panoptic,metrics}.cpp
+// against the minimal Eigen stand-in in oracle/eigen_min (see its headers for the numerics
+// they keep).
 // TEST INFRASTRUCTURE ONLY: tests/ use it to pin oracle/oracle.cpp (and, through it,
 // the GPU path) to the reference's actual code; bench.py --impl reference times it as
 // the reference CPU renderer. The product library never links it.
@@ -13,6 +14,8 @@
 #include <vector>
 
 #include "psimap/core_types.hpp"
+#include "psimap/metrics.hpp"
+#include "psimap/panoptic.hpp"
 #include "psimap/raster.hpp"
 #include "psimap/synthetic.hpp"
 
@@ -288,6 +291,75 @@ int ref_bench_render(void* h, const psm_camera* cam, int32_t reps, const psm_ras
       o[0] = b.time_ms; o[1] = b.fps; o[2] = static_cast<double>(b.rn_total); o[3] = b.rn_per_tile;
       o[4] = static_cast<double>(b.blended_total); o[5] = b.blended_per_pixel;
     }
+  } catch (const std::invalid_argument&) {
+    return PSM_EINVAL;
+  }
+  return PSM_OK;
+}
+
+// ---- panoptic rows (F1, F2)
+
+namespace {
+// SceneMap with f_sem, f_ins and the instance queries (feature, mean, cov column-major,
+// alive, class id), as pack_queries / psm_queries lay them out.
+SceneMap panoptic_scene(const double* surfels13, int64_t n, const double* f_sem, int32_t c_sem, const double* f_ins,
+                        int32_t c_ins, int32_t n_queries, const double* q_feat, const double* q_mean,
+                        const double* q_cov, const int32_t* q_alive, const int32_t* q_class) {
+  SceneMap sc;
+  sc.surfels.resize(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    Surfel& sf = sc.surfels[i];
+    sf = to_surfel(surfels13 + 13 * i);
+    sf.f_sem = VecX(c_sem);
+    for (int c = 0; c < c_sem; ++c) sf.f_sem[c] = f_sem[i * c_sem + c];
+    sf.f_ins = VecX(c_ins);
+    for (int c = 0; c < c_ins; ++c) sf.f_ins[c] = f_ins[i * c_ins + c];
+  }
+  for (int q = 0; q < n_queries; ++q) {
+    InstanceQuery iq;
+    iq.feature = VecX(c_ins);
+    for (int c = 0; c < c_ins; ++c) iq.feature[c] = q_feat[q * c_ins + c];
+    iq.mean = Vec3(q_mean[3 * q], q_mean[3 * q + 1], q_mean[3 * q + 2]);
+    for (int c = 0; c < 3; ++c)
+      for (int r = 0; r < 3; ++r) iq.cov(r, c) = q_cov[9 * q + 3 * c + r];
+    iq.alive = q_alive[q] != 0;
+    iq.class_id = q_class ? q_class[q] : -1;
+    sc.queries.push_back(iq);
+  }
+  return sc;
+}
+}  // namespace
+
+// assign_labels (panoptic.cpp:36-91): dist_out n x n_queries (per-surfel rows), argmax_out n.
+int ref_assign_labels(const double* surfels13, int64_t n, const double* f_ins, int32_t c_ins, int32_t n_queries,
+                      const double* q_feat, const double* q_mean, const double* q_cov, const int32_t* q_alive,
+                      double* dist_out, int32_t* argmax_out) {
+  try {
+    const SceneMap sc = panoptic_scene(surfels13, n, nullptr, 0, f_ins, c_ins, n_queries, q_feat, q_mean, q_cov,
+                                       q_alive, nullptr);
+    const LabelAssignment la = assign_labels(sc.queries, nullptr, sc);
+    for (int64_t s = 0; s < n; ++s) {
+      for (int q = 0; q < n_queries; ++q) dist_out[s * n_queries + q] = la.dist(q, s);
+      argmax_out[s] = la.argmax[s];
+    }
+  } catch (const std::invalid_argument&) {
+    return PSM_EINVAL;
+  }
+  return PSM_OK;
+}
+
+// render_panoptic (metrics.cpp:339-369): ids / classes / sem_classes planes (W*H int32).
+int ref_render_panoptic(const double* surfels13, int64_t n, const double* f_sem, int32_t c_sem, const double* f_ins,
+                        int32_t c_ins, int32_t n_queries, const double* q_feat, const double* q_mean,
+                        const double* q_cov, const int32_t* q_alive, const int32_t* q_class, const psm_camera* cam,
+                        const psm_raster_config* cfg, int32_t* ids, int32_t* classes, int32_t* sem_classes) {
+  try {
+    const SceneMap sc = panoptic_scene(surfels13, n, f_sem, c_sem, f_ins, c_ins, n_queries, q_feat, q_mean, q_cov,
+                                       q_alive, q_class);
+    const PanopticRender pr = render_panoptic(sc, to_cam(cam), to_cfg(cfg));
+    put(ids, pr.ids);
+    put(classes, pr.classes);
+    put(sem_classes, pr.sem_classes);
   } catch (const std::invalid_argument&) {
     return PSM_EINVAL;
   }

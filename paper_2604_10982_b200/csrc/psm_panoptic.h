@@ -10,12 +10,14 @@
 // covariance, retried with an eps*I floor when it is not positive definite
 // (panoptic.cpp:53-62).
 //
-// Evaluation order: dot products and 3x3 products are left-to-right sums; the LLT is
-// Eigen's unblocked lower algorithm (llt_inplace::unblocked) with its solve against
-// the identity. Eigen's own vectorised reductions may associate differently, so the
-// agreement with an Eigen build of the reference is tolerance-level (pinned by
-// test_panoptic.cpp:86-183, ported in tests/test_panoptic_oracle.py); GPU and oracle
-// agree bit for bit. exp is psm_exp (glibc-exact); compile without contraction.
+// Evaluation order is Eigen 3.4's on x86-64 SSE2 without FMA: the feature dot is a
+// dynamic-size vectorised reduction (psm_dot_dyn), the 3x3 products are left-to-right
+// sums, the LLT is llt_inplace::unblocked and its solve against the identity goes
+// through triangular_solve_matrix (psm_llt3_inverse). tests/test_ref_pin.py checks the
+// oracle against the reference's panoptic.cpp / metrics.cpp compiled in oracle/_ref
+// (with oracle/eigen_min modelling the same Eigen code paths); the reference's
+// test_panoptic.cpp:86-183 cases are ported in tests/test_panoptic_oracle.py. GPU and
+// oracle agree bit for bit. exp is psm_exp (glibc-exact); compile without contraction.
 #ifndef PSM_PANOPTIC_H
 #define PSM_PANOPTIC_H
 
@@ -44,7 +46,7 @@ PSM_PHD int psm_llt3(const double* a, double* l) {
     double x = a[k * 3 + k];
     if (k == 1) x -= l[0 * 3 + 1] * l[0 * 3 + 1];
     if (k == 2) x -= l[0 * 3 + 2] * l[0 * 3 + 2] + l[1 * 3 + 2] * l[1 * 3 + 2];
-    if (!(x > 0.0)) return 0;
+    if (x <= 0.0) return 0;  // llt_inplace::unblocked's test (a NaN pivot passes, as there)
     x = sqrt(x);
     l[k * 3 + k] = x;
     for (int i = k + 1; i < 3; ++i) {
@@ -57,21 +59,58 @@ PSM_PHD int psm_llt3(const double* a, double* l) {
   return 1;
 }
 
-// X = (L L^T)^-1 by forward then backward substitution against the identity.
+// X = (L L^T)^-1 = llt.solve(Identity) in Eigen's order: a 3x3 right-hand side goes
+// through triangular_solve_matrix, column by column. Lower solve (L column-major):
+// x_i *= 1 / l_ii, then x_r -= x_i l_ri below it. Upper solve (L^T, row-major) from the
+// last row up: b = 0 + sum over the solved rows in column order, x_i = (x_i - b) / l_ii
+// as a multiply by the reciprocal.
 PSM_PHD void psm_llt3_inverse(const double* l, double* inv) {
-  const double l00 = l[0], l10 = l[1], l20 = l[2], l11 = l[4], l21 = l[5], l22 = l[8];
   for (int c = 0; c < 3; ++c) {
-    const double e0 = c == 0 ? 1.0 : 0.0, e1 = c == 1 ? 1.0 : 0.0, e2 = c == 2 ? 1.0 : 0.0;
-    const double y0 = e0 / l00;
-    const double y1 = (e1 - l10 * y0) / l11;
-    const double y2 = (e2 - l20 * y0 - l21 * y1) / l22;
-    const double x2 = y2 / l22;
-    const double x1 = (y1 - l21 * x2) / l11;
-    const double x0 = (y0 - l10 * x1 - l20 * x2) / l00;
-    inv[c * 3 + 0] = x0;
-    inv[c * 3 + 1] = x1;
-    inv[c * 3 + 2] = x2;
+    double x[3] = {c == 0 ? 1.0 : 0.0, c == 1 ? 1.0 : 0.0, c == 2 ? 1.0 : 0.0};
+    for (int i = 0; i < 3; ++i) {
+      const double a = 1.0 / l[i * 3 + i];
+      x[i] = x[i] * a;
+      for (int r = i + 1; r < 3; ++r) x[r] = x[r] - x[i] * l[i * 3 + r];
+    }
+    for (int k = 0; k < 3; ++k) {
+      const int i = 2 - k;
+      const double a = 1.0 / l[i * 3 + i];
+      double b = 0.0;
+      for (int t = 0; t < k; ++t) b = b + l[i * 3 + (i + 1 + t)] * x[i + 1 + t];
+      x[i] = (x[i] - b) * a;
+    }
+    inv[c * 3 + 0] = x[0];
+    inv[c * 3 + 1] = x[1];
+    inv[c * 3 + 2] = x[2];
   }
+}
+
+// VectorXd::dot in Eigen's order (redux_impl, LinearVectorizedTraversal, NoUnrolling,
+// 2-wide packets, aligned start): the products accumulate in two packet sums over
+// 4-element strides, one more packet when two remain, the two lanes are added, then
+// the odd tail.
+PSM_PHD double psm_dot_dyn(const double* a, const double* b, int n) {
+  const int aligned = (n / 2) * 2, aligned2 = (n / 4) * 4;
+  if (!aligned) return n > 0 ? a[0] * b[0] : 0.0;
+  double p0 = a[0] * b[0], p1 = a[1] * b[1];
+  if (aligned > 2) {
+    double q0 = a[2] * b[2], q1 = a[3] * b[3];
+    for (int i = 4; i < aligned2; i += 4) {
+      p0 = p0 + a[i] * b[i];
+      p1 = p1 + a[i + 1] * b[i + 1];
+      q0 = q0 + a[i + 2] * b[i + 2];
+      q1 = q1 + a[i + 3] * b[i + 3];
+    }
+    p0 = p0 + q0;
+    p1 = p1 + q1;
+    if (aligned > aligned2) {
+      p0 = p0 + a[aligned2] * b[aligned2];
+      p1 = p1 + a[aligned2 + 1] * b[aligned2 + 1];
+    }
+  }
+  double res = p0 + p1;
+  for (int i = aligned; i < n; ++i) res = res + a[i] * b[i];
+  return res;
 }
 
 // Sigma^-1 of a query covariance (panoptic.cpp:53-62), column-major in and out.
@@ -98,9 +137,7 @@ PSM_PHD int psm_assign_one(const double* f_ins, int c_ins, const double* center,
                            const uint64_t* tab) {
   double a_max = -1;
   for (int a = 0; a < n_alive; ++a) {
-    double dot = 0.0;
-    for (int c = 0; c < c_ins; ++c) dot = dot + fq[a * c_ins + c] * f_ins[c];
-    const double sim = psm_sigmoid_t(dot, tab);
+    const double sim = psm_sigmoid_t(psm_dot_dyn(fq + a * c_ins, f_ins, c_ins), tab);
     const double d0 = center[0] - mean[a * 3 + 0];
     const double d1 = center[1] - mean[a * 3 + 1];
     const double d2 = center[2] - mean[a * 3 + 2];

@@ -199,3 +199,52 @@ def test_stage_functions_are_reference():
             w[: m // 3] = w[0]  # ties broken by proj ascending
             p = np.array([int(rng.uniform_int(1000)) for _ in range(m)], np.int32)
             assert np.array_equal(R.topk_select(w, p, k), O.topk_select(w, p, k))
+
+
+# ---- panoptic rows (F1 assign_labels, F2 render_panoptic): panoptic.cpp / metrics.cpp compiled in _ref
+def _panoptic_street(n=12000, w=256, h=192, c_sem=32, n_queries=24):
+    from paper_2604_10982_b200 import street_f_ins, street_queries
+    spec = StreetSpec(n_surfels=n, image_w=w, image_h=h, c_sem=c_sem, seed=7)
+    sc, _, cam = make_street_scene(spec, with_labels=False)
+    qs = street_queries(n_queries, c_ins=8)
+    qs[3].alive = False
+    qs[11].alive = False
+    return SceneMap(sc.surfels, sc.f_sem, street_f_ins(spec), qs), cam
+
+
+def test_assign_labels_is_reference():
+    """The oracle's assign_labels (psm_panoptic.h, shared with the GPU) equals the reference's bit for bit:
+    Eigen's dynamic dot order, LLT and its triangular solve as modelled by oracle/eigen_min."""
+    sc, _ = _panoptic_street()
+    rd, ra = R.assign_labels(sc.surfels, sc.f_ins, sc.queries)
+    od, oa = O.assign_labels(sc.surfels, sc.f_ins, sc.queries)
+    assert np.array_equal(ra, oa)
+    assert np.array_equal(rd.view(np.uint64), od.view(np.uint64))
+    # odd feature widths and non-trivial covariances (the LLT retry, the dot's tail)
+    from paper_2604_10982_b200 import InstanceQuery
+    rng = np.random.default_rng(1)
+    for c_ins in (1, 3, 5, 8, 13, 16):
+        f = rng.standard_normal((500, c_ins))
+        qs = []
+        for i in range(9):
+            a = rng.standard_normal((3, 3))
+            cov = a @ a.T + (0.0 if i == 4 else 0.1) * np.eye(3)
+            if i == 6:
+                cov = np.diag([1.0, 1.0, 0.0])  # not positive definite: the eps retry
+            qs.append(InstanceQuery(rng.standard_normal(c_ins), rng.uniform(-2, 2, 3), cov, alive=i != 2))
+        s = np.zeros((500, 13))
+        s[:, :3] = rng.uniform(-3, 3, (500, 3))
+        s[:, 3] = 1.0
+        rd, ra = R.assign_labels(s, f, qs)
+        od, oa = O.assign_labels(s, f, qs)
+        assert np.array_equal(ra, oa) and np.array_equal(rd.view(np.uint64), od.view(np.uint64)), c_ins
+
+
+@pytest.mark.parametrize("blending,k", [(Blending.TopK, 16), (Blending.Full, 16), (Blending.TopK, 8)])
+def test_render_panoptic_is_reference(blending, k):
+    sc, cam = _panoptic_street()
+    cfg = RasterConfig(binning=Binning.Aabb, blending=blending, top_k=k)
+    r = R.render_panoptic(sc, cam, cfg)
+    o = O.render_panoptic(sc, sc.f_ins, sc.queries, cam, cfg)
+    for key in ("ids", "classes", "sem_classes"):
+        assert np.array_equal(r[key], o[key]), key
