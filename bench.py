@@ -446,7 +446,10 @@ def run_ours(args):
                    "l2": "flushed between timed steps (256 MB write outside the events)",
                    "views_per_rank_per_step": len(cams),
                    "parallelism": f"view-sharded x{world}, scene replicated",
-                   "stage_ms": stage_avg, "alg_bytes_per_frame": b_frame},
+                   "stage_ms": stage_avg, "alg_bytes_per_frame": b_frame,
+                   **({"stage_ms_note": "batch: event spans of the last view of each step; its stages share the "
+                                        "GPU with the other context's view, so front-end spans include waits "
+                                        "(tile_scan most)"} if batch else {})},
         "roofline": {"bound": "hbm", "kernel": "blend_kernel (K7)", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src, "alg_bytes_per_launch": b_blend, "launch_ms": blend_avg},
