@@ -490,6 +490,21 @@ int oracle_project_surfel(const double* s13, const psm_camera* cam, double chi2,
   return 1;
 }
 
+// project_surfel_backward (raster.cpp:179-203) of one surfel under its own projection, through
+// the shared psm_geom_backward: g_hinv row-major in; returns the projection status.
+int oracle_project_surfel_backward(const double* s13, const psm_camera* pcam, double chi2, const double* g_hinv,
+                                   double* d_center, double* d_rot, double* d_scales) {
+  const Cam cam = cam_from(pcam);
+  Projected p;
+  const int st = project_surfel(s13, cam, chi2, p);
+  if (st != 1) return st;
+  double hinv[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) hinv[r * 3 + c] = p.h_inv.at(r, c);
+  psm_geom_backward(s13, cam.r.m, hinv, g_hinv, d_center, d_rot, d_scales);
+  return 1;
+}
+
 // sample_surfel_alpha + evaluate_alpha, raster.cpp:154-177
 double oracle_evaluate_alpha(const double* s13, const psm_camera* pcam, double px, double py,
                              const psm_raster_config* cfg, double* u_out, double* v_out, double* w2_out,
@@ -683,7 +698,108 @@ struct BackwardAcc {
   const psm_plane_grads* g;
   std::vector<double> opacity, color, fsem, lab, hinv;  // per source; hinv per projected (row-major)
   std::vector<double> center, rotation, scales;         // per source
+  std::vector<std::vector<Scratch::Entry>> rows;        // per pixel: the forward's contributors
 };
+
+// Blending backward (pipeline.cpp:347-460) in the reference's summation order: the pixels in
+// kGradChunks = 16 linear ranges, each summed (pixel order) into its own zeroed buffers, the
+// buffers then added to the totals in chunk order (pipeline.cpp:355-376,455-463). With that
+// order the sums are the reference's bit for bit (tests/test_ref_pin.py).
+static void blend_backward(BackwardAcc* bwd, const double* surfels13, const double* f_sem, int c_sem,
+                           const double* labels, int n_q, const Cam& cam, const psm_raster_config* cfg,
+                           const std::vector<Projected>& projected, int n) {
+  const int n_proj = static_cast<int>(projected.size());
+  const int64_t total_px = static_cast<int64_t>(cam.w) * cam.h;
+  const bool topk = cfg->blending == PSM_BLEND_TOPK;
+  const int k_sel = std::max(cfg->top_k, 1);
+  constexpr int kGradChunks = 16;
+  bwd->hinv.assign(static_cast<size_t>(n_proj) * 9, 0.0);
+  std::vector<double> b_hinv, b_op, b_col, b_fsem, b_lab;
+  std::vector<double> t_chain, wbuf;
+  std::vector<WeightKey> keys, best;
+  std::vector<char> selected;
+  for (int c = 0; c < kGradChunks; ++c) {
+    b_hinv.assign(static_cast<size_t>(n_proj) * 9, 0.0);
+    b_op.assign(static_cast<size_t>(n), 0.0);
+    b_col.assign(static_cast<size_t>(n) * 3, 0.0);
+    b_fsem.assign(static_cast<size_t>(n) * c_sem, 0.0);
+    b_lab.assign(static_cast<size_t>(n) * n_q, 0.0);
+    for (int64_t pix = total_px * c / kGradChunks; pix < total_px * (c + 1) / kGradChunks; ++pix) {
+      const auto& ent = bwd->rows[pix];
+      const int m = static_cast<int>(ent.size());
+      if (m == 0) continue;
+      const int x = static_cast<int>(pix % cam.w), y = static_cast<int>(pix / cam.w);
+      const double rx = (x + 0.5 - cam.cx) / cam.fx, ry = (y + 0.5 - cam.cy) / cam.fy;
+      const double zero3[3] = {0, 0, 0};
+      const double* gc = bwd->g->color ? bwd->g->color + 3 * pix : zero3;
+      const double* gf = (c_sem > 0 && bwd->g->sem_feat) ? bwd->g->sem_feat + pix * c_sem : nullptr;
+      const double* gi = (n_q > 0 && bwd->g->ins_dist) ? bwd->g->ins_dist + pix * n_q : nullptr;
+      t_chain.assign(m + 1, 1.0);
+      wbuf.assign(m, 0.0);
+      for (int j = 0; j < m; ++j) {
+        wbuf[j] = ent[j].alpha * t_chain[j];
+        t_chain[j + 1] = t_chain[j] * (1.0 - ent[j].alpha);
+      }
+      if (topk && m > k_sel) {  // the forward's Top-K selection, replayed (pipeline.cpp:383-388)
+        keys.resize(m);
+        for (int i = 0; i < m; ++i) keys[i] = {wbuf[i], ent[i].proj, i};
+        topk_select(keys.data(), m, k_sel, best, selected);
+      } else {
+        selected.assign(m, 1);
+      }
+      double suffix = t_chain[m] * (gc[0] * cfg->background[0] + gc[1] * cfg->background[1] + gc[2] * cfg->background[2]);
+      for (int j = m - 1; j >= 0; --j) {
+        const auto& e = ent[j];
+        const int64_t src = projected[e.proj].source;
+        const double* sf = surfels13 + 13 * src;
+        const double w_j = wbuf[j];
+        double direct = gc[0] * sf[10] + gc[1] * sf[11] + gc[2] * sf[12];
+        for (int k = 0; k < 3; ++k) b_col[src * 3 + k] += w_j * gc[k];
+        if (selected[j]) {
+          if (gf) {
+            double dot = 0;
+            for (int i = 0; i < c_sem; ++i) {
+              dot += gf[i] * f_sem[src * c_sem + i];
+              b_fsem[src * c_sem + i] += w_j * gf[i];
+            }
+            direct += dot;
+          }
+          if (gi) {
+            double dot = 0;
+            for (int i = 0; i < n_q; ++i) {
+              dot += gi[i] * labels[src * n_q + i];
+              b_lab[src * n_q + i] += w_j * gi[i];
+            }
+            direct += dot;
+          }
+        }
+        const double one_minus = 1.0 - e.alpha;
+        const double g_alpha = t_chain[j] * direct - (one_minus > 0 ? suffix / one_minus : 0.0);
+        suffix += w_j * direct;
+        const double d_sigma = oexp(-0.5 * (e.u * e.u + e.v * e.v));
+        b_op[src] += d_sigma * g_alpha;
+        const double g_dsigma = sf[9] * g_alpha;
+        const double g_u = -e.u * d_sigma * g_dsigma;
+        const double g_v = -e.v * d_sigma * g_dsigma;
+        const Projected& pr = projected[e.proj];
+        const double w2 = pr.h_inv.at(2, 0) * rx + pr.h_inv.at(2, 1) * ry + pr.h_inv.at(2, 2) * 1.0;
+        const double gw[3] = {g_u / w2, g_v / w2, -(e.u * g_u + e.v * g_v) / w2};
+        const double ray[3] = {rx, ry, 1.0};
+        double* gh = &b_hinv[static_cast<size_t>(e.proj) * 9];
+        for (int r = 0; r < 3; ++r)
+          for (int k = 0; k < 3; ++k) gh[r * 3 + k] += gw[r] * ray[k];
+      }
+    }
+    // deterministic ordered merge (pipeline.cpp:455-463)
+    for (size_t i = 0; i < b_hinv.size(); ++i) bwd->hinv[i] += b_hinv[i];
+    for (int64_t s2 = 0; s2 < n; ++s2) {
+      bwd->opacity[s2] += b_op[s2];
+      for (int k = 0; k < 3; ++k) bwd->color[s2 * 3 + k] += b_col[s2 * 3 + k];
+    }
+    for (size_t i = 0; i < b_fsem.size(); ++i) bwd->fsem[i] += b_fsem[i];
+    for (size_t i = 0; i < b_lab.size(); ++i) bwd->lab[i] += b_lab[i];
+  }
+}
 
 static int render_impl(const double* surfels13, int64_t n, const double* f_sem, int32_t c_sem,
                        const double* labels, int32_t n_q, const psm_camera* pcam, const psm_raster_config* cfg_in,
@@ -759,7 +875,7 @@ static int render_impl(const double* surfels13, int64_t n, const double* f_sem, 
       hot_normal[static_cast<size_t>(i) * 3 + c] = pr.normal_vis[c];
     }
   }
-  if (bwd) bwd->hinv.assign(static_cast<size_t>(n_proj) * 9, 0.0);
+  if (bwd) bwd->rows.assign(npx, {});
   const double rd_bg0 = cfg->background[0], rd_bg1 = cfg->background[1], rd_bg2 = cfg->background[2];
   std::vector<std::vector<std::pair<int, double>>> cache_rows(cache ? npx : 0);
   const bool rdn = cfg->render_depth_normal != 0;
@@ -856,61 +972,7 @@ static int render_impl(const double* surfels13, int64_t n, const double* f_sem, 
             for (int i = 0; i < k_sel; ++i) slot[i] = i < blend_n ? projected[blend_list[i].proj].source : -1;
           }
 
-          if (bwd && m > 0) {  // blending backward over this pixel (pipeline.cpp:378-453)
-            const double* gc = bwd->g->color ? bwd->g->color + 3 * pix : nullptr;
-            const double* gf = (c_sem > 0 && bwd->g->sem_feat) ? bwd->g->sem_feat + pix * c_sem : nullptr;
-            const double* gi = (n_q > 0 && bwd->g->ins_dist) ? bwd->g->ins_dist + pix * n_q : nullptr;
-            const double zero3[3] = {0, 0, 0};
-            if (!gc) gc = zero3;
-            std::vector<double> t_chain(m + 1, 1.0), wbuf(m);
-            for (int j = 0; j < m; ++j) {
-              wbuf[j] = scratch.entries[j].alpha * t_chain[j];
-              t_chain[j + 1] = t_chain[j] * (1.0 - scratch.entries[j].alpha);
-            }
-            const bool sel_all = !(topk && m > k_sel);
-            double suffix = t_chain[m] * (gc[0] * rd_bg0 + gc[1] * rd_bg1 + gc[2] * rd_bg2);
-            for (int j = m - 1; j >= 0; --j) {
-              const auto& e = scratch.entries[j];
-              const int64_t src = projected[e.proj].source;
-              const double* sf = surfels13 + 13 * src;
-              const double w_j = wbuf[j];
-              double direct = gc[0] * sf[10] + gc[1] * sf[11] + gc[2] * sf[12];
-              for (int c = 0; c < 3; ++c) bwd->color[src * 3 + c] += w_j * gc[c];
-              if (sel_all || scratch.selected[j]) {
-                if (gf) {
-                  double dot = 0;
-                  for (int i = 0; i < c_sem; ++i) {
-                    dot += gf[i] * f_sem[src * c_sem + i];
-                    bwd->fsem[src * c_sem + i] += w_j * gf[i];
-                  }
-                  direct += dot;
-                }
-                if (gi) {
-                  double dot = 0;
-                  for (int i = 0; i < n_q; ++i) {
-                    dot += gi[i] * labels[src * n_q + i];
-                    bwd->lab[src * n_q + i] += w_j * gi[i];
-                  }
-                  direct += dot;
-                }
-              }
-              const double one_minus = 1.0 - e.alpha;
-              const double g_alpha = t_chain[j] * direct - (one_minus > 0 ? suffix / one_minus : 0.0);
-              suffix += w_j * direct;
-              const double d_sigma = oexp(-0.5 * (e.u * e.u + e.v * e.v));
-              bwd->opacity[src] += d_sigma * g_alpha;
-              const double g_dsigma = sf[9] * g_alpha;
-              const double g_u = -e.u * d_sigma * g_dsigma;
-              const double g_v = -e.v * d_sigma * g_dsigma;
-              const HotGeom& hg = hot_geom[e.proj];
-              const double w2 = hg.h[6] * rx + hg.h[7] * ry + hg.h[8];
-              const double gw[3] = {g_u / w2, g_v / w2, -(e.u * g_u + e.v * g_v) / w2};
-              const double ray[3] = {rx, ry, 1.0};
-              double* gh = &bwd->hinv[static_cast<size_t>(e.proj) * 9];
-              for (int r = 0; r < 3; ++r)
-                for (int c = 0; c < 3; ++c) gh[r * 3 + c] += gw[r] * ray[c];
-            }
-          }
+          if (bwd) bwd->rows[pix] = scratch.entries;  // the RenderCache row (raster.cpp:399-403)
 
           const int feat_dims = c_sem + n_q;
           blends += blend_n;
@@ -954,7 +1016,9 @@ static int render_impl(const double* surfels13, int64_t n, const double* f_sem, 
   });
   const auto t3 = clk::now();
 
-  if (bwd) {  // project_surfel_backward per projected surfel (pipeline.cpp:478-486)
+  if (bwd) {  // blending backward, then project_surfel_backward per projected surfel (pipeline.cpp:478-486)
+    blend_backward(bwd, surfels13, f_sem, c_sem, labels, n_q, cam, cfg, projected, static_cast<int>(n));
+    bwd->rows.clear();
     bwd->center.assign(static_cast<size_t>(n) * 3, 0.0);
     bwd->rotation.assign(static_cast<size_t>(n) * 4, 0.0);
     bwd->scales.assign(static_cast<size_t>(n) * 2, 0.0);

@@ -60,6 +60,8 @@ def load(libm: bool = False):
     lib.oracle_bin.restype = C.c_int
     lib.oracle_bin.argtypes = [vp, C.c_int64, P(A.psm_camera), P(A.psm_raster_config), C.c_int32, C.c_double,
                                vp, vp, C.c_int64, vp, P(A.psm_counters)]
+    lib.oracle_project_surfel_backward.restype = C.c_int
+    lib.oracle_project_surfel_backward.argtypes = [vp, P(A.psm_camera), C.c_double, vp, vp, vp, vp]
     lib.oracle_topk_select.restype = None
     lib.oracle_topk_select.argtypes = [vp, vp, C.c_int32, C.c_int32, vp]
     _libs[key] = lib
@@ -88,6 +90,18 @@ def project_surfel(s13, cam, chi2: float = 9.0) -> dict:
         "footprint_inv": np.array(list(out.finv)).reshape(2, 2).T,
         "normal_vis": np.array(list(out.normal_vis)),
     }
+
+
+def project_surfel_backward(s13, cam, g_hinv, chi2: float = 9.0) -> Optional[dict]:
+    """project_surfel_backward (raster.cpp:179-203) through psm_geom_backward: d L / d (centre,
+    quaternion, scales) from d L / d H^-1 (3x3). None when the surfel does not project."""
+    s = np.ascontiguousarray(np.asarray(s13, dtype=np.float64).reshape(13))
+    g = np.ascontiguousarray(np.asarray(g_hinv, dtype=np.float64).reshape(3, 3))
+    dc, dq, ds = np.zeros(3), np.zeros(4), np.zeros(2)
+    st = load().oracle_project_surfel_backward(_p(s), C.byref(cam.to_c()), chi2, _p(g), _p(dc), _p(dq), _p(ds))
+    if st < 0:
+        raise ValueError("degenerate quaternion")
+    return None if st == 0 else {"center": dc, "rotation": dq, "scales": ds}
 
 
 def evaluate_alpha(s13, cam, px: float, py: float, cfg) -> dict:

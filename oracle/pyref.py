@@ -1,6 +1,7 @@
 """ctypes wrapper of oracle/_ref/libpsimap_ref.so: the REFERENCE'S OWN render path
-(/root/reference/proj/src/{raster,math_util,core_types,synthetic}.cpp) and panoptic rows
-(panoptic.cpp assign_labels, metrics.cpp render_panoptic), compiled unchanged by
+(/root/reference/proj/src/{raster,math_util,core_types,synthetic}.cpp), the panoptic rows
+(panoptic.cpp assign_labels, metrics.cpp render_panoptic) and the backward row (pipeline.cpp
+pipeline_backward with losses.cpp / sogmm.cpp, raster.cpp project_surfel_backward), compiled unchanged by
 oracle/ref/Makefile against the minimal Eigen stand-in oracle/eigen_min.
 TEST INFRASTRUCTURE ONLY: imported by tests/ and by bench.py's reference arm, never by
 the product package.
@@ -74,6 +75,10 @@ def load():
         "ref_assign_labels": (C.c_int, [vp, C.c_int64, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp]),
         "ref_render_panoptic": (C.c_int, [vp, C.c_int64, vp, C.c_int32, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp,
                                           P(A.psm_camera), P(A.psm_raster_config), vp, vp, vp]),
+        "ref_project_surfel_backward": (C.c_int, [vp, P(A.psm_camera), P(A.psm_raster_config), vp, vp, vp, vp]),
+        "ref_pipeline_backward": (C.c_int, [vp, P(A.psm_camera), P(A.psm_raster_config), C.c_int32, vp, vp,
+                                            C.c_double, C.c_double, C.c_double, C.c_double, P(A.psm_scene_grads),
+                                            vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -174,6 +179,40 @@ class RefScene:
         if self.lib.ref_bench_render(self.h, C.byref(cam.to_c()), reps, C.byref(cfg.to_c()), _p(rows)) != 0:
             raise ValueError("degenerate quaternion")
         return rows
+
+
+    def pipeline_backward(self, cam, cfg, rgb_gt, sem_gt=None, lambda_s=0.2, l_rgb=1.0, l_sem=0.5, l_iso=0.0,
+                          smooth=False) -> dict:
+        """pipeline_backward (pipeline.cpp:253-600) of this query-free scene with no SOGMM model:
+        the surfel gradients (psm_scene_grads fields, per-surfel rows) and "g_color_plane", the colour
+        gradient the reference fed its blending backward (loss_rgb_backward, pipeline.cpp:266)."""
+        A = _abi()
+        n = self.surfels.shape[0]
+        out = {"opacity": np.zeros(n), "color": np.zeros((n, 3)), "f_sem": np.zeros((n, self.c_sem)),
+               "center": np.zeros((n, 3)), "rotation": np.zeros((n, 4)), "scales": np.zeros((n, 2)),
+               "g_color_plane": np.zeros((cam.height, cam.width, 3))}
+        sg = A.psm_scene_grads(_p(out["opacity"]), _p(out["color"]), _p(out["f_sem"]), None, _p(out["center"]),
+                               _p(out["rotation"]), _p(out["scales"]))
+        rgb = np.ascontiguousarray(np.asarray(rgb_gt, dtype=np.float64).reshape(cam.height, cam.width, 3))
+        sem = None if sem_gt is None else np.ascontiguousarray(np.asarray(sem_gt, dtype=np.int32).reshape(-1))
+        st = self.lib.ref_pipeline_backward(self.h, C.byref(cam.to_c()), C.byref(cfg.to_c()), int(smooth), _p(rgb),
+                                            _p(sem), lambda_s, l_rgb, l_sem, l_iso, C.byref(sg),
+                                            _p(out["g_color_plane"]))
+        if st != 0:
+            raise ValueError("degenerate quaternion")
+        return out
+
+
+def project_surfel_backward(s13, cam, cfg, g_hinv) -> Optional[dict]:
+    """project_surfel_backward (raster.cpp:179-203) under the surfel's own projection; None if culled."""
+    s = np.ascontiguousarray(np.asarray(s13, dtype=np.float64).reshape(13))
+    g = np.ascontiguousarray(np.asarray(g_hinv, dtype=np.float64).reshape(3, 3))
+    dc, dq, ds = np.zeros(3), np.zeros(4), np.zeros(2)
+    st = load().ref_project_surfel_backward(_p(s), C.byref(cam.to_c()), C.byref(cfg.to_c()), _p(g), _p(dc), _p(dq),
+                                            _p(ds))
+    if st < 0:
+        raise ValueError("degenerate quaternion")
+    return None if st == 0 else {"center": dc, "rotation": dq, "scales": ds}
 
 
 def project_surfel(s13, cam, cfg) -> Optional[dict]:

@@ -1,5 +1,5 @@
 // ref_capi.cpp — C-ABI over the REFERENCE'S OWN render path, compiled unchanged from
-// /root/reference/proj/src/{raster,math_util,core_types,synthetic,panoptic,metrics}.cpp
+// /root/reference/proj/src/{raster,math_util,core_types,synthetic,panoptic,metrics,losses,sogmm,pipeline}.cpp
 // against the minimal Eigen stand-in in oracle/eigen_min (see its headers for the numerics
 // they keep).
 // TEST INFRASTRUCTURE ONLY: tests/ use it to pin oracle/oracle.cpp (and, through it,
@@ -14,8 +14,10 @@
 #include <vector>
 
 #include "psimap/core_types.hpp"
+#include "psimap/losses.hpp"
 #include "psimap/metrics.hpp"
 #include "psimap/panoptic.hpp"
+#include "psimap/pipeline.hpp"
 #include "psimap/raster.hpp"
 #include "psimap/synthetic.hpp"
 
@@ -360,6 +362,84 @@ int ref_render_panoptic(const double* surfels13, int64_t n, const double* f_sem,
     put(ids, pr.ids);
     put(classes, pr.classes);
     put(sem_classes, pr.sem_classes);
+  } catch (const std::invalid_argument&) {
+    return PSM_EINVAL;
+  }
+  return PSM_OK;
+}
+
+// ---- backward row (F4)
+
+// project_surfel_backward (raster.cpp:179-203) of one surfel under its own projection:
+// g_hinv row-major 3x3 in; d_center[3], d_rotation[4] (w, x, y, z), d_scales[2] out.
+// Returns 1 (projected), 0 (culled, outputs untouched) or -1 (degenerate quaternion).
+int ref_project_surfel_backward(const double* s13, const psm_camera* pcam, const psm_raster_config* pcfg,
+                                const double* g_hinv, double* d_center, double* d_rotation, double* d_scales) {
+  const Surfel sf = to_surfel(s13);
+  const Camera cam = to_cam(pcam);
+  try {
+    auto p = project_surfel(sf, cam, to_cfg(pcfg));
+    if (!p.has_value()) return 0;
+    Mat3 g;
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) g(r, c) = g_hinv[3 * r + c];
+    const SurfelGeomGrads gg = project_surfel_backward(sf, cam, *p, g);
+    for (int k = 0; k < 3; ++k) d_center[k] = gg.d_center[k];
+    for (int k = 0; k < 4; ++k) d_rotation[k] = gg.d_rotation[k];
+    for (int k = 0; k < 2; ++k) d_scales[k] = gg.d_scales[k];
+  } catch (const std::invalid_argument&) {
+    return -1;
+  }
+  return 1;
+}
+
+// pipeline_backward (pipeline.cpp:253-600) of a scene without queries and without a SOGMM
+// model, under the loss weights given (l_geo and l_ins have no terms here; pass l_iso = 0
+// to leave only the render's gradients): the frame is (camera, rgb_gt W*H*3, sem_gt W*H or
+// NULL). smooth != 0 uses PipelineConfig::smooth()'s raster settings (pipeline.cpp:56-64)
+// instead of *pcfg. Outputs (each may be NULL): the scene gradients in psm_scene_grads
+// layout, and the colour-plane gradient the reference fed its blending backward
+// (loss_rgb_backward of the forward colour, pipeline.cpp:266).
+int ref_pipeline_backward(void* h, const psm_camera* pcam, const psm_raster_config* pcfg, int32_t smooth,
+                          const double* rgb_gt, const int32_t* sem_gt, double lambda_s, double l_rgb, double l_sem,
+                          double l_iso, psm_scene_grads* out, double* g_color_plane) {
+  auto* r = static_cast<RefScene*>(h);
+  const Camera cam = to_cam(pcam);
+  PipelineConfig cfg = smooth ? PipelineConfig::smooth() : PipelineConfig{};
+  if (!smooth) cfg.raster = to_cfg(pcfg);
+  cfg.raster.threads = pcfg->threads;
+  cfg.weights.lambda_s = lambda_s;
+  cfg.weights.l_rgb = l_rgb;
+  cfg.weights.l_sem = l_sem;
+  cfg.weights.l_iso = l_iso;
+  FrameBundle frame;
+  frame.camera = cam;
+  frame.rgb = Image(cam.width, cam.height, 3);
+  std::memcpy(frame.rgb.data.data(), rgb_gt, sizeof(double) * frame.rgb.data.size());
+  if (sem_gt) {
+    frame.sem_gt = IntPlane(cam.width, cam.height, 1);
+    std::memcpy(frame.sem_gt.data.data(), sem_gt, sizeof(int32_t) * frame.sem_gt.data.size());
+  }
+  try {
+    const BackwardResult bw = pipeline_backward(r->scene, nullptr, frame, cfg);
+    const Gradients& g = bw.grads;
+    const int64_t n = static_cast<int64_t>(r->scene.surfels.size());
+    const int c_sem = r->scene.c_sem();
+    for (int64_t s = 0; s < n; ++s) {
+      if (out->opacity) out->opacity[s] = g.opacity[s];
+      for (int k = 0; k < 3; ++k) {
+        if (out->color) out->color[3 * s + k] = g.color[s][k];
+        if (out->center) out->center[3 * s + k] = g.center[s][k];
+      }
+      for (int k = 0; k < 4 && out->rotation; ++k) out->rotation[4 * s + k] = g.rotation[s][k];
+      for (int k = 0; k < 2 && out->scales; ++k) out->scales[2 * s + k] = g.scales[s][k];
+      for (int c = 0; c < c_sem && out->f_sem; ++c) out->f_sem[s * c_sem + c] = g.f_sem(c, s);
+    }
+    if (g_color_plane) {
+      const RenderTargets t = render(r->scene, nullptr, cam, cfg.raster);
+      const Image gc = loss_rgb_backward(t.color, frame.rgb, lambda_s, l_rgb);
+      std::memcpy(g_color_plane, gc.data.data(), sizeof(double) * gc.data.size());
+    }
   } catch (const std::invalid_argument&) {
     return PSM_EINVAL;
   }

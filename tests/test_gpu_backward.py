@@ -1,6 +1,7 @@
 """GPU render backward against the oracle backward (which the
-finite-difference suite in tests/test_backward_oracle.py pins): every gradient within fp64
-summation-order noise (the GPU sums per-surfel contributions with atomics)."""
+finite-difference suite in tests/test_backward_oracle.py pins, and tests/test_ref_pin.py pins bit
+for bit to the reference's own pipeline_backward): every gradient within fp64 summation-order noise
+(the GPU sums per-surfel contributions with atomics)."""
 import numpy as np
 import pytest
 

@@ -7,7 +7,9 @@ bin_circle / bin_aabb (raster.cpp:51-90,144-152), the bench_render counters
 (raster.cpp:513-573), the stage functions (project_surfel, evaluate_alpha, topk_select), the
 street-scene generator (synthetic.cpp:236-312) and Camera::look_at (core_types.cpp:40-60).
 Non-identity camera poses (the C5 trajectory, an arbitrary Camera::make pose) exercise the
-camera transform products (raster.cpp:96-101, core_types.hpp:51-52) bit for bit.
+camera transform products (raster.cpp:96-101, core_types.hpp:51-52) bit for bit. The panoptic
+rows (panoptic.cpp assign_labels, metrics.cpp render_panoptic) and the backward row
+(raster.cpp project_surfel_backward, pipeline.cpp pipeline_backward) are pinned the same way.
 
 The oracle's parity build uses psm_exp (the GPU's exp); the libm build uses glibc exp like
 the reference. Both must match the reference exactly: psm_exp restates glibc's FMA exp.
@@ -248,3 +250,84 @@ def test_render_panoptic_is_reference(blending, k):
     o = O.render_panoptic(sc, sc.f_ins, sc.queries, cam, cfg)
     for key in ("ids", "classes", "sem_classes"):
         assert np.array_equal(r[key], o[key]), key
+
+
+# ---- backward row (F4): raster.cpp project_surfel_backward and pipeline.cpp pipeline_backward in _ref
+def test_project_surfel_backward_is_reference():
+    """project_surfel_backward (raster.cpp:179-203) vs psm_geom_backward (the oracle's and the GPU's),
+    bit for bit, under non-identity poses."""
+    rng = Rng(11)
+    cams = _pose_cameras(320, 240)
+    cfg = RasterConfig()
+    projected = 0
+    for i in range(300):
+        c = cams[i % len(cams)]
+        q = rng.unit_quaternion()
+        s13 = np.array([rng.uniform(-3, 3), rng.uniform(-2, 2), rng.uniform(-1, 25), *q, rng.uniform(0.01, 1.5),
+                        rng.uniform(0.01, 0.4), rng.uniform(0.1, 1), 0.5, 0.5, 0.5])
+        g = np.array([rng.uniform(-1, 1) for _ in range(9)]).reshape(3, 3)
+        r, o = R.project_surfel_backward(s13, c, cfg, g), O.project_surfel_backward(s13, c, g, cfg.chi2)
+        assert (r is None) == (o is None)
+        if r is None:
+            continue
+        projected += 1
+        for k in r:
+            assert np.array_equal(r[k], o[k]), (i, k)
+    assert projected > 150
+
+
+def sem_ce_plane_grad(sem_feat, sem_gt, l_sem):
+    """d L_sem / d sem_feat of the clamped cross-entropy as pipeline_backward forms it
+    (pipeline.cpp:270-295); math.exp is the C library's exp, like the reference's std::exp."""
+    h, w, c_sem = sem_feat.shape
+    g = np.zeros_like(sem_feat)
+    labeled = int((sem_gt >= 0).sum())
+    if labeled == 0:
+        return g
+    scale = l_sem / labeled
+    for y in range(h):
+        for x in range(w):
+            cls = int(sem_gt[y, x])
+            if cls < 0:
+                continue
+            f = sem_feat[y, x]
+            m = f[0]
+            for i in range(1, c_sem):
+                m = max(m, f[i])
+            den = 0.0
+            for i in range(c_sem):
+                den += math.exp(f[i] - m)
+            p_cls = math.exp(f[cls] - m) / den
+            if p_cls < 1e-7 or p_cls > 1.0 - 1e-7:
+                continue
+            for i in range(c_sem):
+                g[y, x, i] = scale * (math.exp(f[i] - m) / den - (1.0 if i == cls else 0.0))
+    return g
+
+
+SMOOTH = RasterConfig(alpha_min=0.0, t_min=0.0, support_cutoff=False, chi2=1e8, blending=Blending.Full)  # pipeline.cpp:56-64
+
+
+@pytest.mark.parametrize("case", ["topk4", "full", "smooth"])
+def test_pipeline_backward_is_reference(case):
+    """The oracle's blending backward + geometry chain (oracle_render_backward) against the reference's own
+    pipeline_backward (pipeline.cpp:253-600) on a query-free scene without a SOGMM model and l_iso = 0, so
+    that every surfel gradient comes from the render: the upstream colour plane is the reference's own
+    loss_rgb_backward, the semantic plane its clamped cross-entropy (restated above). Bit for bit: the
+    oracle sums in the reference's 16 pixel chunks, merged in order."""
+    sc, _, cam = make_street_scene(StreetSpec(n_surfels=3000, image_w=96, image_h=64, c_sem=6), with_labels=False)
+    rs = R.RefScene(sc.surfels, sc.f_sem, None)
+    rng = np.random.default_rng(3)
+    rgb = rng.uniform(0, 1, (64, 96, 3))
+    sem = rng.integers(-1, 6, (64, 96)).astype(np.int32)
+    cfg = {"topk4": RasterConfig(blending=Blending.TopK, top_k=4), "full": RasterConfig(),
+           "smooth": SMOOTH}[case]
+    pose = _pose_cameras(96, 64)[4]
+    for c in (cam, pose):
+        r = rs.pipeline_backward(c, cfg, rgb, sem, l_sem=0.5, l_iso=0.0, smooth=case == "smooth")
+        g_sem = sem_ce_plane_grad(rs.render(c, cfg)["sem_feat"], sem, 0.5)
+        o = O.render_backward(sc, None, c, cfg, g_color=r["g_color_plane"], g_sem=g_sem)
+        for k in ("opacity", "color", "f_sem", "center", "rotation", "scales"):
+            assert np.count_nonzero(r[k]) > 0, k
+            assert np.array_equal(r[k], o[k]), (case, k, float(np.max(np.abs(r[k] - o[k]))))
+    rs.close()
