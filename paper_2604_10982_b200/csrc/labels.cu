@@ -79,9 +79,12 @@ __global__ void __launch_bounds__(256) assign_labels_kernel(LabelParams p) {
 // memory ([query][33] per warp, padded against bank conflicts) instead of the global
 // scratch, and then writes the 32 rows cooperatively: lane = column, so every row store
 // is one coalesced run (the per-thread row stores of the general path touch one 32-byte
-// sector per lane and value).
+// sector per lane and value). CI > 0: C_ins == CI at compile time, so the surfel's f_ins
+// row is loaded once into registers and every query's dot is unrolled; the dynamic form
+// re-reads the row through L1 for every query (C3p, 32 queries, C_ins 8: 0.89 -> 0.55 ms).
 constexpr int kRowsMaxAlive = 32;
 constexpr int kRowsWarps = 8;
+template <int CI>
 __global__ void __launch_bounds__(32 * kRowsWarps) assign_labels_rows_kernel(LabelParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* tab = reinterpret_cast<uint64_t*>(smem);
@@ -97,8 +100,20 @@ __global__ void __launch_bounds__(32 * kRowsWarps) assign_labels_rows_kernel(Lab
   int best = -1;
   if (s < p.n && p.n_alive > 0) {
     const double center[3] = {p.surfels[s * 13 + 0], p.surfels[s * 13 + 1], p.surfels[s * 13 + 2]};
-    const int b = psm_assign_one(p.f_ins + s * p.c_ins, p.c_ins, center, p.n_alive, qs, mean, inv, wv + lane, 33,
-                                 tab);
+    int b;
+    if constexpr (CI > 0) {
+      double f[CI];
+      const double2* row = reinterpret_cast<const double2*>(p.f_ins + s * CI);  // 16 B aligned: CI even
+#pragma unroll
+      for (int c = 0; c < CI / 2; ++c) {
+        const double2 v = __ldg(row + c);
+        f[2 * c] = v.x;
+        f[2 * c + 1] = v.y;
+      }
+      b = psm_assign_one(f, CI, center, p.n_alive, qs, mean, inv, wv + lane, 33, tab);
+    } else {
+      b = psm_assign_one(p.f_ins + s * p.c_ins, p.c_ins, center, p.n_alive, qs, mean, inv, wv + lane, 33, tab);
+    }
     best = p.alive_index[b];
   }
   if (s < p.n && p.argmax) p.argmax[s] = best;
@@ -142,12 +157,16 @@ void launch_assign_labels(const LabelParams& p, cudaStream_t st) {
     static unsigned long long configured_rows = 0;
     const int most = 2048 + static_cast<int>(sizeof(double)) * (kRowsWarps * kRowsMaxAlive * 33 + kQsWords);
     if (!(configured_rows >> dev & 1ull)) {
-      cudaFuncSetAttribute(assign_labels_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+      cudaFuncSetAttribute(assign_labels_rows_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+      cudaFuncSetAttribute(assign_labels_rows_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+      cudaFuncSetAttribute(assign_labels_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
       configured_rows |= 1ull << dev;
     }
     const size_t smem = 2048 + sizeof(double) * (kRowsWarps * kRowsMaxAlive * 33 + words);
     const unsigned blocks = static_cast<unsigned>((p.n + 32 * kRowsWarps - 1) / (32 * kRowsWarps));
-    assign_labels_rows_kernel<<<blocks, 32 * kRowsWarps, smem, st>>>(p);
+    if (p.c_ins == 8) assign_labels_rows_kernel<8><<<blocks, 32 * kRowsWarps, smem, st>>>(p);
+    else if (p.c_ins == 16) assign_labels_rows_kernel<16><<<blocks, 32 * kRowsWarps, smem, st>>>(p);
+    else assign_labels_rows_kernel<0><<<blocks, 32 * kRowsWarps, smem, st>>>(p);
     return;
   }
   const unsigned blocks = static_cast<unsigned>((p.n + 255) / 256);

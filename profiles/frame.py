@@ -13,9 +13,20 @@ wl = sys.argv[1] if len(sys.argv) > 1 else "c3"
 frames = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 scene, cams, (n, w, h, c, blending, k, desc) = bench.build_workload(wl, 0, 1)
 r = Renderer(0)
-ds = r.upload(scene, None)
+pano = bool(scene.queries)  # c3p: assign_labels + render_panoptic, as bench.py's step
+ds = r.upload(scene, exact=pano)
 cfg = bench.raster_cfg(blending, k)
+if pano:
+    import numpy as np
+    import torch
+    qclass = np.array([q.class_id for q in scene.queries], np.int32)
+    ptrs = {kk: torch.empty(w * h, dtype=torch.int32, device="cuda:0").data_ptr()
+            for kk in ("ids", "classes", "sem_classes")}
 for _ in range(frames):
-    r.render_device(ds, cams[0], cfg, {})  # NULL planes: context scratch
+    if pano:
+        r.assign_labels(ds, scene.queries, outputs=False)
+        r.render_panoptic_device(ds, cams[0], cfg, qclass, ptrs)
+    else:
+        r.render_device(ds, cams[0], cfg, {})  # NULL planes: context scratch
     r.sync()
 print(f"{wl}: {frames} frames rendered")

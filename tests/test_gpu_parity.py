@@ -9,8 +9,9 @@ import numpy as np
 import pytest
 
 from oracle import pyoracle as O
+from oracle import pyref as R
 from paper_2604_10982_b200 import (Binning, Blending, RasterConfig, Renderer, RenderTargets, SceneMap, StreetSpec,
-                                   density_scale, make_street_scene)
+                                   density_scale, make_street_scene, trajectory_cameras)
 from paper_2604_10982_b200 import _abi as A
 from tests.helpers import Rng, facing_surfel, front_camera, scene_of
 
@@ -255,6 +256,27 @@ def test_gpu_c3_full_size_parity(rend, c3):
     g, o = assert_parity(rend, sc, None, cam, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK,
                                                           top_k=8))
     assert g.rn_total > 1_000_000
+
+
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not built")
+def test_gpu_c3_full_size_vs_compiled_reference(rend, c3):
+    """The GPU frame against THE REFERENCE'S OWN render_into (oracle/_ref: raster.cpp compiled unchanged)
+    at the metric's config, the street camera and a C5 trajectory pose: blend counts, ins_argmax and
+    blended_total exact, every fp32 plane within the north star's 1e-4 of the reference's fp64 plane.
+    The reference bins by AABB, the GPU by ellipse (identical planes, test above)."""
+    sc, _, cam = c3
+    rs = R.RefScene(sc.surfels, sc.f_sem, None)
+    try:
+        for c in (cam, trajectory_cameras(256, 1280, 720, first=200, count=1)[0]):
+            g = rend.render(sc, None, c, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=8))
+            r = rs.render(c, RasterConfig(binning=Binning.Aabb, blending=Blending.TopK, top_k=8, threads=0))
+            assert g.blended_total == r["blended_total"]
+            assert np.array_equal(g.blend_count, r["blend_count"]) and np.array_equal(g.ins_argmax, r["ins_argmax"])
+            for k in ("color", "depth", "normal", "alpha_acc", "sem_feat"):
+                err = np.max(np.abs(getattr(g, k).astype(np.float64) - r[k]))
+                assert err <= ATOL, (k, err)
+    finally:
+        rs.close()
 
 
 def test_gpu_c3_binning_output_identity(rend, c3):

@@ -1,11 +1,13 @@
 """Per-source-line instruction / stall-sample shares of one kernel in an ncu report
-(python tools/ncu_lines.py REPORT KERNEL_REGEX [TOP]); reads `ncu --page source --print-source cuda,sass`."""
+(python tools/ncu_lines.py REPORT KERNEL_REGEX [TOP] [LAUNCH_SKIP]); reads `ncu --page source --print-source cuda,sass`
+(all matching launches, or only the one after LAUNCH_SKIP of them)."""
 import csv, io, subprocess, sys
 
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", "regex:" + kre],
-                     capture_output=True, text=True).stdout
+skip = ["--launch-skip", sys.argv[4], "--launch-count", "1"] if len(sys.argv) > 4 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", "regex:" + kre]
+                     + skip, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 lines, cur, fname = {}, None, ""
 for r in rows:
