@@ -720,41 +720,68 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     const bool gate = inside && (planes || !(1.0 - T < 0.5));
     int nsel = blend_n;
     if constexpr (FULL_LIST) nsel = nsel < p.list_cap ? nsel : p.list_cap;
-    for (int q = 0; q < 32; ++q) {
+    // kLP lanes per pixel, 32 / kLP pixels per iteration: with at most 128 channels, two
+    // pixels share the warp (8 channels per lane), which doubles the rows in flight per
+    // iteration and halves the argmax reductions per pixel
+    constexpr int kLP = PANO_T <= 4 ? 16 : 32;
+    constexpr int kPPI = 32 / kLP;
+    constexpr int kCPL = PANO_T * 32 / kLP;  // channels per lane: c = sub + kLP * t
+    const int grp = lane / kLP, sub = lane % kLP;
+    for (int q0 = 0; q0 < 32; q0 += kPPI) {
+      const int q = q0 + grp;
       const int qx = wx0 + blk_px(q), qy = wy0 + blk_py(q);
       const bool qgate = __shfl_sync(0xffffffffu, gate, q);
       const int nq = __shfl_sync(0xffffffffu, nsel, q);
       const int64_t qpix = static_cast<int64_t>(qy) * p.width + qx;
-      if (!qgate) {
-        if (lane == 0 && qx < p.width && qy < p.height && !planes) {
-          p.pan_ids[qpix] = -1;
-          p.pan_classes[qpix] = -1;
-          p.pan_sem[qpix] = -1;
-        }
-        continue;
+      if (!qgate && sub == 0 && qx < p.width && qy < p.height && !planes) {
+        p.pan_ids[qpix] = -1;
+        p.pan_classes[qpix] = -1;
+        p.pan_sem[qpix] = -1;
       }
-      double acc[PANO_T];
+      if (!__any_sync(0xffffffffu, qgate)) continue;
+      double acc[kCPL];
 #pragma unroll
-      for (int t = 0; t < PANO_T; ++t) acc[t] = 0.0;
+      for (int t = 0; t < kCPL; ++t) acc[t] = 0.0;
       if constexpr (KMAX > 0) {
-        // lane i < nq fetches slot i's source and weight; the rows are then loaded back to
-        // back and summed in blend order
-        const int i_l = lane < KMAX ? lane : 0;
-        int src = 0;
-        double sw = 0.0;
-        if (lane < nq && D > 0) {
-          src = static_cast<int>(__ldg(p.vals + top_p[i_l * kCT + (tid & ~31) + q]));
-          sw = top_w[i_l * kCT + (tid & ~31) + q];
+        // lane sub fetches slot i0 + sub's source and weight; the rows are then loaded back
+        // to back and summed in blend order
+        constexpr int kRound = KMAX < kLP ? KMAX : kLP;
+#pragma unroll
+        for (int i0 = 0; i0 < KMAX; i0 += kRound) {
+          const int si = i0 + sub;
+          int src = 0;
+          double sw = 0.0;
+          if (qgate && sub < kRound && si < nq && D > 0) {
+            src = static_cast<int>(__ldg(p.vals + top_p[si * kCT + (tid & ~31) + q]));
+            sw = top_w[si * kCT + (tid & ~31) + q];
+          }
+#pragma unroll
+          for (int i = 0; i < kRound; ++i) {
+            const int s_i = __shfl_sync(0xffffffffu, src, grp * kLP + i);
+            const double w = __shfl_sync(0xffffffffu, sw, grp * kLP + i);
+            if (qgate && i0 + i < nq && D > 0) {
+              const double* row = p.feat64 + static_cast<int64_t>(s_i) * D;
+#pragma unroll
+              for (int t = 0; t < kCPL; ++t) {
+                const int c = sub + kLP * t;
+                if (c < D) {
+                  const double v = __ldg(row + c);
+                  acc[t] = i0 + i == 0 ? w * v : acc[t] + w * v;
+                }
+              }
+            }
+          }
         }
+      } else {
+        const int n_all = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(qgate && D > 0 ? nq : 0)));
+        for (int i = 0; i < n_all; ++i) {
+          if (qgate && i < nq) {
+            const int pos = static_cast<int>(p.lists[qpix * p.list_cap + i].x);
+            const double w = p.lists_w[qpix * p.list_cap + i];
+            const double* row = p.feat64 + static_cast<int64_t>(__ldg(p.vals + pos)) * D;
 #pragma unroll
-        for (int i = 0; i < KMAX; ++i) {
-          const int s_i = __shfl_sync(0xffffffffu, src, i);
-          const double w = __shfl_sync(0xffffffffu, sw, i);
-          if (i < nq && D > 0) {
-            const double* row = p.feat64 + static_cast<int64_t>(s_i) * D;
-#pragma unroll
-            for (int t = 0; t < PANO_T; ++t) {
-              const int c = lane + 32 * t;
+            for (int t = 0; t < kCPL; ++t) {
+              const int c = sub + kLP * t;
               if (c < D) {
                 const double v = __ldg(row + c);
                 acc[t] = i == 0 ? w * v : acc[t] + w * v;
@@ -762,44 +789,55 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
             }
           }
         }
-      } else {
-        for (int i = 0; i < (D > 0 ? nq : 0); ++i) {
-          const int pos = static_cast<int>(p.lists[qpix * p.list_cap + i].x);
-          const double w = p.lists_w[qpix * p.list_cap + i];
-          const double* row = p.feat64 + static_cast<int64_t>(__ldg(p.vals + pos)) * D;
-#pragma unroll
-          for (int t = 0; t < PANO_T; ++t) {
-            const int c = lane + 32 * t;
-            if (c < D) {
-              const double v = __ldg(row + c);
-              acc[t] = i == 0 ? w * v : acc[t] + w * v;
-            }
-          }
-        }
       }
-      // first-max argmaxes over the semantic (c < cs) and label (c >= cs) channels
+      // first-max argmaxes over the semantic (c < cs) and label (cs <= c < D) channels: the
+      // maximum by a butterfly within the pixel's lanes, then the lowest channel holding it
       double bs = 0.0, bi = 0.0;
-      int ks = 0x7fffffff, ki = 0x7fffffff;
+      bool hs = false, hi = false;
 #pragma unroll
-      for (int t = 0; t < PANO_T; ++t) {
-        const int c = lane + 32 * t;
+      for (int t = 0; t < kCPL; ++t) {
+        const int c = sub + kLP * t;
         if (c < cs) {
-          if (ks == 0x7fffffff || acc[t] > bs) { bs = acc[t]; ks = c; }
+          if (!hs || acc[t] > bs) bs = acc[t];
+          hs = true;
         } else if (c < D) {
-          if (ki == 0x7fffffff || acc[t] > bi) { bi = acc[t]; ki = c - cs; }
+          if (!hi || acc[t] > bi) bi = acc[t];
+          hi = true;
         }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
+      for (int o = kLP / 2; o > 0; o >>= 1) {
         const double os = __shfl_xor_sync(0xffffffffu, bs, o), oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        const int oks = __shfl_xor_sync(0xffffffffu, ks, o), oki = __shfl_xor_sync(0xffffffffu, ki, o);
-        if (oks != 0x7fffffff && (ks == 0x7fffffff || os > bs || (os == bs && oks < ks))) { bs = os; ks = oks; }
-        if (oki != 0x7fffffff && (ki == 0x7fffffff || oi > bi || (oi == bi && oki < ki))) { bi = oi; ki = oki; }
+        const bool ohs = __shfl_xor_sync(0xffffffffu, hs, o), ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+        if (ohs && (!hs || os > bs)) bs = os;
+        if (ohi && (!hi || oi > bi)) bi = oi;
+        hs = hs || ohs;
+        hi = hi || ohi;
       }
+      unsigned fs = 0xffffffffu, fi = 0xffffffffu;  // this lane's lowest channel holding the maximum
+#pragma unroll
+      for (int t = kCPL - 1; t >= 0; --t) {
+        const int c = sub + kLP * t;
+        if (c < cs && acc[t] == bs) fs = static_cast<unsigned>(c);
+        else if (c >= cs && c < D && acc[t] == bi) fi = static_cast<unsigned>(c - cs);
+      }
+      int ks, ki;
+      if constexpr (kLP == 32) {
+        ks = static_cast<int>(__reduce_min_sync(0xffffffffu, fs));
+        ki = static_cast<int>(__reduce_min_sync(0xffffffffu, fi));
+      } else {
+        const unsigned s0 = __reduce_min_sync(0xffffffffu, grp == 0 ? fs : 0xffffffffu);
+        const unsigned s1 = __reduce_min_sync(0xffffffffu, grp == 1 ? fs : 0xffffffffu);
+        const unsigned i0 = __reduce_min_sync(0xffffffffu, grp == 0 ? fi : 0xffffffffu);
+        const unsigned i1 = __reduce_min_sync(0xffffffffu, grp == 1 ? fi : 0xffffffffu);
+        ks = static_cast<int>(grp == 0 ? s0 : s1);
+        ki = static_cast<int>(grp == 0 ? i0 : i1);
+      }
+      if (!qgate) continue;
       if (planes) {  // raster.cpp:486-498: zeros (and -1) where nothing blended
 #pragma unroll
-        for (int t = 0; t < PANO_T; ++t) {
-          const int c = lane + 32 * t;
+        for (int t = 0; t < kCPL; ++t) {
+          const int c = sub + kLP * t;
           const float v = nq > 0 ? static_cast<float>(acc[t]) : 0.f;
           if (c < cs) {
             if (p.sem_feat) p.sem_feat[qpix * cs + c] = v;
@@ -807,10 +845,10 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
             if (p.ins_dist) p.ins_dist[qpix * p.n_q + (c - cs)] = v;
           }
         }
-        if (lane == 0) p.ins_argmax[qpix] = (p.n_q > 0 && nq > 0) ? ki : -1;
+        if (sub == 0) p.ins_argmax[qpix] = (p.n_q > 0 && nq > 0) ? ki : -1;
         continue;
       }
-      if (lane == 0) {
+      if (sub == 0) {
         // ins_argmax stays -1 without labels or blends (raster.cpp:292,497); the
         // semantic plane is all zeros when nothing blended, whose first max is 0
         const int id = (p.n_q > 0 && nq > 0) ? ki : -1;
