@@ -32,11 +32,32 @@
 #include <math.h>
 #endif
 
-// sigmoid (math_util.cpp:122-128)
+// psm_exp_t with its common range unbranched: psm_exp_main always, the full function only
+// when the argument is outside it (psm_exp_main_ok); same value as psm_exp_t(x, tab).
+PSM_PHD double psm_exp_q(double x, const uint64_t* tab) {
+  double y = psm_exp_main(x, tab);
+  if (!psm_exp_main_ok(x)) y = psm_exp_t(x, tab);
+  return y;
+}
+
+// Which exps of assign_labels take psm_exp_q: bit 0 the sigmoid's, bit 1 the softmax's,
+// bit 2 the Mahalanobis term's (the others psm_exp_t; the values are identical). C3p
+// (32 queries), frames/s with the branch-free sigmoid: none 434, sigmoid 445, sigmoid +
+// softmax 442, all three 456.
+#ifndef PSM_LABEL_EXPQ
+#define PSM_LABEL_EXPQ 7
+#endif
+PSM_PHD double psm_label_exp(double x, const uint64_t* tab, int which) {
+  return (PSM_LABEL_EXPQ >> which & 1) ? psm_exp_q(x, tab) : psm_exp_t(x, tab);
+}
+
+// sigmoid (math_util.cpp:122-128): x >= 0: 1 / (1 + exp(-x)), else e / (1 + e) with
+// e = exp(x). One exp and one division whatever the sign, so that a warp whose lanes
+// disagree on it does not run both branches.
 PSM_PHD double psm_sigmoid_t(double x, const uint64_t* tab) {
-  if (x >= 0) return 1.0 / (1.0 + psm_exp_t(-x, tab));
-  const double e = psm_exp_t(x, tab);
-  return e / (1.0 + e);
+  const bool pos = x >= 0;
+  const double e = psm_label_exp(pos ? -x : x, tab, 0);
+  return (pos ? 1.0 : e) / (1.0 + e);
 }
 
 // Lower Cholesky of a symmetric 3x3 (column-major a[c*3 + r]); 0 if not positive definite.
@@ -146,7 +167,7 @@ PSM_PHD int psm_assign_one(const double* f_ins, int c_ins, const double* center,
     const double v1 = (m[1] * d0 + m[4] * d1) + m[7] * d2;
     const double v2 = (m[2] * d0 + m[5] * d1) + m[8] * d2;
     const double q = (d0 * v0 + d1 * v1) + d2 * v2;
-    const double geo = psm_exp_t(-0.5 * q, tab);
+    const double geo = psm_label_exp(-0.5 * q, tab, 2);
     const double av = sim * geo;
     a_vals[a * a_stride] = av;
     a_max = av > a_max ? av : a_max;  // std::max(a_max, av)
@@ -162,7 +183,7 @@ PSM_PHD int psm_assign_one(const double* f_ins, int c_ins, const double* center,
       best = a;
       best_a = av;
     }
-    const double e = psm_exp_t(av - a_max, tab);
+    const double e = psm_label_exp(av - a_max, tab, 1);
     a_vals[a * a_stride] = e;
     denom += e;
   }
