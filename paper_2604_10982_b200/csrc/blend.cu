@@ -723,7 +723,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     // kLP lanes per pixel, 32 / kLP pixels per iteration: with at most 128 channels, two
     // pixels share the warp (8 channels per lane), which doubles the rows in flight per
     // iteration and halves the argmax reductions per pixel
-    constexpr int kLP = PANO_T <= 4 ? 16 : 32;
+    constexpr int kLP = PANO_T <= 3 ? 8 : (PANO_T <= 4 ? 16 : 32);
     constexpr int kPPI = 32 / kLP;
     constexpr int kCPL = PANO_T * 32 / kLP;  // channels per lane: c = sub + kLP * t
     const int grp = lane / kLP, sub = lane % kLP;
@@ -825,13 +825,14 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       if constexpr (kLP == 32) {
         ks = static_cast<int>(__reduce_min_sync(0xffffffffu, fs));
         ki = static_cast<int>(__reduce_min_sync(0xffffffffu, fi));
-      } else {
-        const unsigned s0 = __reduce_min_sync(0xffffffffu, grp == 0 ? fs : 0xffffffffu);
-        const unsigned s1 = __reduce_min_sync(0xffffffffu, grp == 1 ? fs : 0xffffffffu);
-        const unsigned i0 = __reduce_min_sync(0xffffffffu, grp == 0 ? fi : 0xffffffffu);
-        const unsigned i1 = __reduce_min_sync(0xffffffffu, grp == 1 ? fi : 0xffffffffu);
-        ks = static_cast<int>(grp == 0 ? s0 : s1);
-        ki = static_cast<int>(grp == 0 ? i0 : i1);
+      } else {  // minimum within the pixel's lanes
+#pragma unroll
+        for (int o = kLP / 2; o > 0; o >>= 1) {
+          fs = min(fs, __shfl_xor_sync(0xffffffffu, fs, o));
+          fi = min(fi, __shfl_xor_sync(0xffffffffu, fi, o));
+        }
+        ks = static_cast<int>(fs);
+        ki = static_cast<int>(fi);
       }
       if (!qgate) continue;
       if (planes) {  // raster.cpp:486-498: zeros (and -1) where nothing blended
@@ -945,6 +946,7 @@ void launch_pano(const BlendParams& p, int tiles, cudaStream_t st) {
   const int t = (p.feat_dims + 31) / 32;
   if (t <= 1) launch_t<KMAX, FULL, 1, 0, 32, true, 1>(p, tiles, st);
   else if (t <= 2) launch_t<KMAX, FULL, 1, 0, 32, true, 2>(p, tiles, st);
+  else if (t <= 3) launch_t<KMAX, FULL, 1, 0, 32, true, 3>(p, tiles, st);
   else if (t <= 4) launch_t<KMAX, FULL, 1, 0, 32, true, 4>(p, tiles, st);
   else if (t <= 8) launch_t<KMAX, FULL, 1, 0, 32, true, 8>(p, tiles, st);
   else launch_t<KMAX, FULL, 1, 0, 32, true, 16>(p, tiles, st);
