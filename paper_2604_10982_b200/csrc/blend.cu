@@ -919,18 +919,22 @@ void launch_t(const BlendParams& p, int tiles, cudaStream_t st) {
   kern<<<grid, cta_threads(KMAX), smem_bytes(KMAX), st>>>(q);
 }
 
-// Feature-lane shapes: float4 lanes, 32/LPP pixels per warp iteration for the
-// common widths; scalar lanes with guards otherwise.
+// Feature-lane shapes: float4 lanes, LPP lanes per pixel (32/LPP pixels per warp
+// iteration), NV float4 per lane, for the common widths; scalar lanes with guards otherwise.
+// Four float4 per lane is the widest that fits the 80-register budget (eight spill); per
+// entry it amortises the slot read and the loop over four times the channels. Measured
+// (blend ms): C3, D = 64: LPP 16 x NV 1 0.800, 8 x 2 0.788, 4 x 4 0.776, 2 x 8 0.822;
+// C4, D = 128: 32 x 1 2.894, 16 x 2 2.814, 8 x 4 2.73, 4 x 8 3.007.
 template <int KMAX, bool FULL>
 void launch_feat(const BlendParams& p, int tiles, cudaStream_t st) {
   const int D = p.feat_dims;
   switch (D) {
     case 0: launch_t<KMAX, FULL, 1, 0, 32, true>(p, tiles, st); return;
-    case 32: launch_t<KMAX, FULL, 4, 1, 8, true>(p, tiles, st); return;
-    case 64: launch_t<KMAX, FULL, 4, 1, 16, true>(p, tiles, st); return;
-    case 96: launch_t<KMAX, FULL, 1, 3, 32, true>(p, tiles, st); return;
-    case 128: launch_t<KMAX, FULL, 4, 1, 32, true>(p, tiles, st); return;
-    case 256: launch_t<KMAX, FULL, 4, 2, 32, true>(p, tiles, st); return;
+    case 32: launch_t<KMAX, FULL, 4, 2, 4, true>(p, tiles, st); return;
+    case 64: launch_t<KMAX, FULL, 4, 4, 4, true>(p, tiles, st); return;
+    case 96: launch_t<KMAX, FULL, 4, 3, 8, true>(p, tiles, st); return;
+    case 128: launch_t<KMAX, FULL, 4, 4, 8, true>(p, tiles, st); return;
+    case 256: launch_t<KMAX, FULL, 4, 4, 16, true>(p, tiles, st); return;
     default: break;
   }
   const int nch = (D + 31) / 32;
