@@ -945,8 +945,11 @@ void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, ui
   const int n_sm = sms[dev];
   // Persistent launches over K3b's class lists. The large classes run on two side streams,
   // concurrently with the many small buckets, which fit beside them on every SM: side:
-  // the beyond-16384 buckets then the 16384-key class (1 CTA per SM each); side2: the
-  // 8192-key class (3 CTAs per SM); main: the <= 1024 then the <= 4096-key classes.
+  // the beyond-16384 buckets (1 CTA per SM) then the 8192-key class (3 CTAs per SM); side2:
+  // the 16384-key class (1 CTA per SM); main: the <= 4096 then the <= 1024-key classes.
+  // The few beyond-16384 buckets hold a handful of SMs for long (C4: 175 us serialised), so
+  // the 16384-key class no longer queues behind them: C4 sort 0.529 -> 0.492 ms (C3, which
+  // has no such buckets, 0.140 -> 0.142); the 8192-key class on the main stream 0.509.
   cudaEventRecord(fork, st);
   cudaStreamWaitEvent(side, fork, 0);
   cudaStreamWaitEvent(side2, fork, 0);
@@ -962,9 +965,9 @@ void launch_sort_tiles(const int32_t* ranges, int tiles, uint64_t* tile_keys, ui
                                                                         classes, tiles);
   }
   launch_sort_class<1024, 3>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
-                             n_sm, side);
+                             n_sm, side2);
   launch_sort_class<1024, 2>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
-                             3 * n_sm, side2);
+                             3 * n_sm, side);
   launch_sort_class<512, 1>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
                             4 * n_sm, st);
   launch_sort_class<PSM_SORT_NT0, 0>(ranges, tiles, tile_keys, tile_vals, tile_masks, depth_bits, depth_minmax, src_bits, classes,
