@@ -113,3 +113,10 @@ def test_gpu_render_panoptic_c3p_full_size(rend):
     assert np.array_equal(g.ids, o["ids"])
     assert np.array_equal(g.classes, o["classes"])
     assert np.array_equal(g.sem_classes, o["sem_classes"])
+    # and directly against THE REFERENCE'S OWN render_panoptic (metrics.cpp:339-369 with
+    # panoptic.cpp's assign_labels and raster.cpp's render, compiled unchanged in oracle/_ref)
+    from oracle import pyref as R
+    if R.available():
+        r = R.render_panoptic(sc, cam, RasterConfig(binning=Binning.Aabb, blending=Blending.TopK, top_k=8))
+        for k in ("ids", "classes", "sem_classes"):
+            assert np.array_equal(getattr(g, k), r[k]), k
