@@ -62,3 +62,31 @@ def test_gpu_backward_zero_upstream(rend):
     scene, lab = scene_case(3)
     g = rend.render_backward(scene, lab, front_camera(32, 32, 60.0), RasterConfig())
     assert all(np.all(v == 0) for v in g.values())
+
+
+@pytest.mark.parametrize("case", ["topk4", "full"])
+def test_gpu_backward_vs_compiled_reference(rend, case):
+    """The GPU backward against THE REFERENCE'S OWN pipeline_backward (pipeline.cpp, compiled unchanged in
+    oracle/_ref) on a query-free scene without a SOGMM model and l_iso = 0: the upstream colour plane is
+    the reference's loss_rgb_backward, the semantic plane its clamped cross-entropy (restated in
+    tests/test_ref_pin.py); every surfel gradient within fp64 summation-order noise."""
+    from oracle import pyref as R
+    from tests.test_ref_pin import _pose_cameras, sem_ce_plane_grad
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    sc, _, cam = make_street_scene(StreetSpec(n_surfels=3000, image_w=96, image_h=64, c_sem=6), with_labels=False)
+    rs = R.RefScene(sc.surfels, sc.f_sem, None)
+    rng = np.random.default_rng(3)
+    rgb = rng.uniform(0, 1, (64, 96, 3))
+    sem = rng.integers(-1, 6, (64, 96)).astype(np.int32)
+    cfg = RasterConfig(blending=Blending.TopK, top_k=4) if case == "topk4" else RasterConfig()
+    try:
+        for c in (cam, _pose_cameras(96, 64)[4]):
+            r = rs.pipeline_backward(c, cfg, rgb, sem, l_sem=0.5, l_iso=0.0)
+            g_sem = sem_ce_plane_grad(rs.render(c, cfg)["sem_feat"], sem, 0.5)
+            g = rend.render_backward(sc, None, c, cfg, r["g_color_plane"], g_sem, None)
+            for k in ("opacity", "color", "f_sem", "center", "rotation", "scales"):
+                scale = max(np.max(np.abs(r[k])), 1e-300)
+                assert np.max(np.abs(g[k] - r[k])) <= 1e-9 * scale, k
+    finally:
+        rs.close()
