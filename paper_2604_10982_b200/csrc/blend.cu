@@ -712,6 +712,9 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
         top_p[(j + 1) * kCT + tid] = pi;
         top_w[(j + 1) * kCT + tid] = wi;
       }
+      // in blend order the positions have served: each lane resolves its slots to source ids
+      // (independent loads, issued back to back) so the pixel loop below reads them directly
+      for (int i = 0; i < blend_n; ++i) top_p[i * kCT + tid] = static_cast<int>(__ldg(p.vals + top_p[i * kCT + tid]));
     }
     __syncwarp();
     const int D = p.feat_dims, cs = p.c_sem;
@@ -752,7 +755,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
           int src = 0;
           double sw = 0.0;
           if (qgate && sub < kRound && si < nq && D > 0) {
-            src = static_cast<int>(__ldg(p.vals + top_p[si * kCT + (tid & ~31) + q]));
+            src = top_p[si * kCT + (tid & ~31) + q];  // resolved above
             sw = top_w[si * kCT + (tid & ~31) + q];
           }
 #pragma unroll
