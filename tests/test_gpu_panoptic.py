@@ -120,3 +120,20 @@ def test_gpu_render_panoptic_c3p_full_size(rend):
         r = R.render_panoptic(sc, cam, RasterConfig(binning=Binning.Aabb, blending=Blending.TopK, top_k=8))
         for k in ("ids", "classes", "sem_classes"):
             assert np.array_equal(getattr(g, k), r[k]), k
+
+
+@pytest.mark.parametrize("c_sem,n_q", [(8, 16), (64, 40), (128, 64), (256, 100), (3, 5)])
+@pytest.mark.parametrize("blending,k", [(Blending.TopK, 8), (Blending.TopK, 32), (Blending.Full, 16)])
+def test_gpu_render_panoptic_feature_widths(rend, c_sem, n_q, blending, k):
+    """The fp64 panoptic phase at every lane shape (8 lanes per pixel up to 96 channels, 16 up to 128,
+    32 beyond; odd widths; Top-K rounds beyond the lanes of a pixel), ids / classes / semantic classes
+    bit-exact vs the oracle."""
+    spec = StreetSpec(n_surfels=4000, image_w=128, image_h=96, c_sem=c_sem, seed=11)
+    scene, _, cam = make_street_scene(spec, with_labels=False)
+    qs = street_queries(n_q, c_ins=8)
+    sc = SceneMap(scene.surfels, scene.f_sem, street_f_ins(spec), qs)
+    cfg = RasterConfig(binning=Binning.Ellipse, blending=blending, top_k=k)
+    g = rend.render_panoptic_scene(sc, cam, cfg)
+    o = O.render_panoptic(sc, sc.f_ins, sc.queries, cam, cfg)
+    for key in ("ids", "classes", "sem_classes"):
+        assert np.array_equal(getattr(g, key), o[key]), key
