@@ -114,30 +114,32 @@ __global__ void __launch_bounds__(256, 3) pixel_backward_kernel(BackwardParams p
   const double* gf = p.c_sem > 0 ? p.g_sem : nullptr;  // kernel parameters: warp-uniform
   const double* gi = p.n_q > 0 ? p.g_ins : nullptr;
   const int cs = p.c_sem, nq = p.n_q, D = cs + nq;
-  const uint2* lst = p.lists + pix * p.list_cap;
-  const double* lt = p.lists_t + pix * p.list_cap;
+  // this pixel's list: entry j at lst[32 j] / lt[32 j] (psm_list_index)
+  const int64_t l0 = inside ? psm_list_index(x, y, p.width, p.list_cap, 0) : 0;
+  const uint2* lst = p.lists + l0;
+  const double* lt = p.lists_t + l0;
 
   // T after the last blend (the forward's chain continued from the stored T_{m-1}),
   // seeding the suffix with the background term
   double suffix = 0.0;
   if (m > 0) {
-    const SurfRec& r = p.recs[__ldg(p.vals + lst[m - 1].x)];
+    const SurfRec& r = p.recs[__ldg(p.vals + lst[32 * (m - 1)].x)];
     const double w0 = r.h[0] * rx + r.h[1] * ry + r.h[2];
     const double w1 = r.h[3] * rx + r.h[4] * ry + r.h[5];
     const double w2 = r.h[6] * rx + r.h[7] * ry + r.h[8];
     const double rcp = 1.0 / w2;
     const double u = w0 * rcp, v = w1 * rcp;
     const double alpha = r.opacity * psm_exp_t(-0.5 * (u * u + v * v), tab);
-    const double t_end = lt[m - 1] * (1.0 - alpha);
+    const double t_end = lt[32 * (m - 1)] * (1.0 - alpha);
     suffix = t_end * (gc0 * p.bg0 + gc1 * p.bg1 + gc2 * p.bg2);
   }
   // the lane's current contributor (position, T before it) and the next one, loaded a
   // step ahead so the walk's max-reduction does not wait on a fresh load
   int j = m - 1;
-  int cur = j >= 0 ? static_cast<int>(lst[j].x) : -1;
-  double tcur = j >= 0 ? lt[j] : 0.0;
-  int nxt = j >= 1 ? static_cast<int>(lst[j - 1].x) : -1;
-  double tnxt = j >= 1 ? lt[j - 1] : 0.0;
+  int cur = j >= 0 ? static_cast<int>(lst[32 * (j)].x) : -1;
+  double tcur = j >= 0 ? lt[32 * (j)] : 0.0;
+  int nxt = j >= 1 ? static_cast<int>(lst[32 * (j - 1)].x) : -1;
+  double tnxt = j >= 1 ? lt[32 * (j - 1)] : 0.0;
   int sp = 0;
   for (;;) {
     const int pos = __reduce_max_sync(0xffffffffu, cur);
@@ -266,8 +268,8 @@ __global__ void __launch_bounds__(256, 3) pixel_backward_kernel(BackwardParams p
       --j;
       cur = nxt;
       tcur = tnxt;
-      nxt = j >= 1 ? static_cast<int>(lst[j - 1].x) : -1;
-      tnxt = j >= 1 ? lt[j - 1] : 0.0;
+      nxt = j >= 1 ? static_cast<int>(lst[32 * (j - 1)].x) : -1;
+      tnxt = j >= 1 ? lt[32 * (j - 1)] : 0.0;
     }
   }
 }

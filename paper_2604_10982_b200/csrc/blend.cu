@@ -247,6 +247,11 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
   int thr_p = 0;        // list position; never compared while thr_w < 0
 
   const int start = p.ranges[2 * tile], end = p.ranges[2 * tile + 1];
+  // this pixel's list entry m is lists[lbase + lstride m]: block-major for the backward
+  // cache (psm_list_index), pixel-major for the Full-mode feature phase
+  const bool cache_lists = p.lists_t != nullptr;
+  const int64_t lbase = !FULL_LIST ? 0 : (cache_lists ? psm_list_index(x, y, p.width, p.list_cap, 0) : pix * p.list_cap);
+  const int lstride = cache_lists ? 32 : 1;
   int* spos = reinterpret_cast<int*>(stage + 2 * kChunk);  // [2][kChunk] list positions of the staged records
   int* ssrc = spos + 2 * kChunk;                           // [2][kChunk] their source ids
   // Top-K slots hold source ids (ties compare them directly, the feature phase reads them
@@ -491,9 +496,10 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
           }
           if constexpr (FULL_LIST) {
             if (m < p.list_cap) {
-              p.lists[pix * p.list_cap + m] = make_uint2(static_cast<uint32_t>(pos), __float_as_uint(wf));
-              if constexpr (PANO_T > 0) p.lists_w[pix * p.list_cap + m] = wt;
-              if (p.lists_t) p.lists_t[pix * p.list_cap + m] = T;  // backward cache: T before this blend
+              const int64_t li = lbase + static_cast<int64_t>(lstride) * m;
+              p.lists[li] = make_uint2(static_cast<uint32_t>(pos), __float_as_uint(wf));
+              if constexpr (PANO_T > 0) p.lists_w[li] = wt;
+              if (p.lists_t) p.lists_t[li] = T;  // backward cache: T before this blend
             }
           }
         }

@@ -261,17 +261,18 @@ int render_impl(psm_ctx* ctx, const psm_scene* sc, const psm_camera* cam, const 
   if (full_list) {
     if (ctx->list_cap == 0) ctx->list_cap = 128;
     uint2* lists;
-    PSM_TRY(ensure(ctx, ctx->lists, npx * ctx->list_cap, &lists));
+    const size_t lslots = static_cast<size_t>(psm_list_slots(W, H, ctx->list_cap));
+    PSM_TRY(ensure(ctx, ctx->lists, lslots, &lists));
     bp.lists = lists;
     bp.list_cap = ctx->list_cap;
     if (pl.pan_ids || planes64) {
       double* lw;
-      PSM_TRY(ensure(ctx, ctx->lists_w, npx * ctx->list_cap, &lw));
+      PSM_TRY(ensure(ctx, ctx->lists_w, lslots, &lw));
       bp.lists_w = lw;
     }
     if (pl.cache) {
       double* lt;
-      PSM_TRY(ensure(ctx, ctx->lists_t, npx * ctx->list_cap, &lt));
+      PSM_TRY(ensure(ctx, ctx->lists_t, lslots, &lt));
       bp.lists_t = lt;
       if (topk) {
         int32_t* tk;

@@ -9,6 +9,22 @@
 
 namespace psm {
 
+// Per-pixel contributor lists (list_cap entries per pixel). Full blending with features
+// keeps them pixel-major (entry m of pixel p at p * cap + m: the feature phase reads one
+// pixel's run back to back). The backward cache keeps them block-major: pixels grouped in
+// the blend's 8x4 blocks, each block's lists entry-major (the 32 pixels' entry m side by
+// side, entry m of a pixel at base + 32 m), so the lanes of a warp, which own one block
+// and advance through their lists at similar rates, store (and the backward loads) a few
+// 256 B runs instead of 32 rows a list apart (C3 cache forward 1.91 -> 1.08 ms).
+__host__ __device__ inline int64_t psm_list_index(int x, int y, int width, int cap, int m) {
+  const int64_t block = static_cast<int64_t>(y >> 2) * ((width + 7) >> 3) + (x >> 3);
+  return (block * cap + m) * 32 + ((y & 3) * 8 + (x & 7));
+}
+// entries a W x H frame's lists occupy in either layout (whole blocks)
+__host__ __device__ inline int64_t psm_list_slots(int width, int height, int cap) {
+  return static_cast<int64_t>((width + 7) >> 3) * ((height + 3) >> 2) * 32 * cap;
+}
+
 struct BlendParams {
   const int32_t* ranges;  // [tiles][2]
   const uint32_t* vals;   // tile-sorted source ids
@@ -28,7 +44,7 @@ struct BlendParams {
   int32_t *ins_argmax, *blend_count;
   unsigned long long* blended_total;
   int32_t* topk_dbg;      // optional [W*H*k_sel]
-  uint2* lists;           // full blending with features: [W*H][list_cap]
+  uint2* lists;           // full blending with features: [W*H][list_cap]; backward cache: psm_list_index
   int32_t list_cap;
   int32_t* list_overflow;
   // panoptic epilogue (render_panoptic, metrics.cpp:339-369): when pan_ids != NULL the

@@ -272,7 +272,7 @@ __global__ void cache_pixels_kernel(const uint2* __restrict__ lists, int list_ca
   const int m = cnt[pix] < list_cap ? cnt[pix] : list_cap;
   int64_t o = offs[pix];
   for (int k = 0; k < m; ++k, ++o) {
-    const uint32_t src = vals[lists[pix * list_cap + k].x];
+    const uint32_t src = vals[lists[psm_list_index(x, y, width, list_cap, k)].x];
     const SurfRec& r = recs[src];
     const double w0 = r.h[0] * rx + r.h[1] * ry + r.h[2];
     const double w1 = r.h[3] * rx + r.h[4] * ry + r.h[5];
