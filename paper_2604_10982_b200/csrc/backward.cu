@@ -23,6 +23,13 @@
 namespace psm {
 namespace {
 
+// candidates owned by at most this many lanes add their terms lane by lane (no reduction).
+// C3 pixel backward (ms): always reduce 3.62-3.66, <= 2 lanes 3.65, 4 3.61, 8 3.56-3.60,
+// 12 3.60-3.62, 16 3.73, always direct 7.0 (fp64 atomics then dominate)
+#ifndef PSM_BWD_DIRECT
+#define PSM_BWD_DIRECT 8
+#endif
+
 // Sum over the warp of 16 per-lane values by recursive halving: after the five steps
 // lane l holds the total of value (l >> 1) (both lanes of a pair hold it). 16 double
 // shuffles instead of 16 x 5 for independent butterflies.
@@ -257,12 +264,23 @@ __global__ void __launch_bounds__(256, 3) pixel_backward_kernel(BackwardParams p
 #pragma unroll
         for (int b = 0; b < 3; ++b) val[4 + a * 3 + b] = gw[a] * ray[b];
     }
-    const double tot = warp_sum16(val, lane);
-    const int k = lane >> 1;
-    if (!(lane & 1) && k < 13) {
-      double* dst = k < 3 ? p.d_color + static_cast<int64_t>(src) * 3 + k
-                          : (k == 3 ? p.d_opacity + src : p.d_hinv + static_cast<int64_t>(src) * 9 + (k - 4));
-      atomicAdd(dst, tot);
+    // few owners: each adds its own 13 terms; otherwise one warp reduction, one atomic each
+    if (__popc(__ballot_sync(0xffffffffu, mine)) <= PSM_BWD_DIRECT) {
+      if (mine) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) atomicAdd(p.d_color + static_cast<int64_t>(src) * 3 + k, val[k]);
+        atomicAdd(p.d_opacity + src, val[3]);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) atomicAdd(p.d_hinv + static_cast<int64_t>(src) * 9 + k, val[4 + k]);
+      }
+    } else {
+      const double tot = warp_sum16(val, lane);
+      const int k = lane >> 1;
+      if (!(lane & 1) && k < 13) {
+        double* dst = k < 3 ? p.d_color + static_cast<int64_t>(src) * 3 + k
+                            : (k == 3 ? p.d_opacity + src : p.d_hinv + static_cast<int64_t>(src) * 9 + (k - 4));
+        atomicAdd(dst, tot);
+      }
     }
     if (mine) {
       --j;
