@@ -274,7 +274,8 @@ struct EmitItem {
 constexpr int kEmitWarps = 8;
 
 // returning atomics in flight per thread (C3 emit, measured: 8 at 4 CTAs/SM 0.098 ms;
-// 8 / 12 / 16 at 3 CTAs 0.112 / 0.113 / 0.131; 16 at 4 CTAs spills, 0.115)
+// 8 / 12 / 16 at 3 CTAs 0.112 / 0.113 / 0.131; 16 at 4 CTAs spills, 0.115; round 2, with
+// the 64 B BinRec: 4 CTAs 0.092, 5 (48 registers, spills) 0.100, 6 (40) 0.120)
 #ifndef PSM_EMIT_BATCH
 #define PSM_EMIT_BATCH 8
 #endif
