@@ -90,3 +90,16 @@ def test_gpu_backward_vs_compiled_reference(rend, case):
                 assert np.max(np.abs(g[k] - r[k])) <= 1e-9 * scale, k
     finally:
         rs.close()
+
+
+@pytest.mark.parametrize("blending,k", [(Blending.Full, 16), (Blending.TopK, 2)])
+def test_gpu_backward_ragged_image(rend, blending, k):
+    """An image whose sides are not multiples of the 8x4 list blocks (block-major cache lists with
+    partial blocks at the right and bottom edges)."""
+    scene, lab = scene_case(7)
+    cam = front_camera(37, 29, 50.0)
+    cfg = RasterConfig(blending=blending, top_k=k)
+    rng = np.random.default_rng(4)
+    gc, gs, gi = rng.normal(size=(29, 37, 3)), rng.normal(size=(29, 37, 3)), rng.normal(size=(29, 37, 2))
+    assert_grads_close(rend.render_backward(scene, lab, cam, cfg, gc, gs, gi),
+                       O.render_backward(scene, lab, cam, cfg, gc, gs, gi))
