@@ -58,7 +58,10 @@ def launches(csv_in, out):
     if not starts:  # captures before the one-kernel frame reset started at preprocess
         starts = [i for i, r in enumerate(rows) if "preprocess_kernel" in r[ki]]
     if starts:  # keep the last frame (from its first launch; memsets are not kernels)
-        rows = rows[starts[-1]:]
+        s0 = starts[-1]
+        if s0 > 0 and "assign_labels" in rows[s0 - 1][ki]:  # render_panoptic frames start at assign_labels
+            s0 -= 1
+        rows = rows[s0:]
     agg = {}
     for r in rows:
         name = r[ki].split("(")[0].replace("void ", "").replace("psm::<unnamed>::", "")
