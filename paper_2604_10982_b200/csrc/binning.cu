@@ -19,6 +19,7 @@
 // re-renders a frame whose RN-Total outgrew them, capi.cu).
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "psm_device.cuh"
 #include "psm_ellipse.h"
@@ -788,21 +789,30 @@ __device__ void sort_huge_bucket(int t, const int32_t* __restrict__ ranges, uint
   constexpr int NT = 1024, E = kHugeChunk / NT;
   uint64_t* src = keys + start;
   uint64_t* dst = scratch + start;
-  for (int c0 = 0; c0 < len; c0 += kHugeChunk) {  // sorted runs of kHugeChunk
-    const int cl = min(kHugeChunk, len - c0);
-    uint64_t v[E];
+  // sorted runs of kHugeChunk; the last, partial run takes the smallest sort that holds it
+  // (a bucket just past 16384 keys otherwise sorts a second full 16384-slot run)
+  auto sort_run = [&](auto e_tag, int c0, int cl) {
+    constexpr int EE = decltype(e_tag)::value;
+    uint64_t v[EE];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int i = threadIdx.x * E + e;
+    for (int e = 0; e < EE; ++e) {
+      const int i = threadIdx.x * EE + e;
       v[e] = i < cl ? src[c0 + i] : ~0ull;
     }
-    merge_sort_regs<NT, E>(v, sm);
+    merge_sort_regs<NT, EE>(v, sm);
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int i = threadIdx.x * E + e;
+    for (int e = 0; e < EE; ++e) {
+      const int i = threadIdx.x * EE + e;
       if (i < cl) src[c0 + i] = v[e];
     }
     __syncthreads();
+  };
+  for (int c0 = 0; c0 < len; c0 += kHugeChunk) {
+    const int cl = min(kHugeChunk, len - c0);
+    if (cl <= 2 * NT) sort_run(std::integral_constant<int, 2>{}, c0, cl);
+    else if (cl <= 4 * NT) sort_run(std::integral_constant<int, 4>{}, c0, cl);
+    else if (cl <= 8 * NT) sort_run(std::integral_constant<int, 8>{}, c0, cl);
+    else sort_run(std::integral_constant<int, E>{}, c0, cl);
   }
   const int per = (len + NT - 1) / NT;  // outputs per thread in each merge pass
   for (int width = kHugeChunk; width < len; width <<= 1) {
