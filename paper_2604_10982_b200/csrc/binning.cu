@@ -176,12 +176,27 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restr
     warp_bucket_slot(lpt_n, lb, t < tiles);
   }
   __syncthreads();
-  if (tid == 0) {
-    int run_b = 0;
-    for (int b = 0; b < kLptBuckets; ++b) {
-      const int c = lpt_n[b];
-      lpt_n[b] = run_b;
-      run_b += c;
+  if (warp == 0) {  // exclusive scan of the bucket counts, kPer consecutive buckets per lane
+    constexpr int kPer = (kLptBuckets + 31) / 32;
+    int x[kPer], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int b = lane * kPer + k;
+      x[k] = b < kLptBuckets ? lpt_n[b] : 0;
+      sum += x[k];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int run_b = incl - sum;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int b = lane * kPer + k;
+      if (b < kLptBuckets) lpt_n[b] = run_b;
+      run_b += x[k];
     }
   }
   __syncthreads();
