@@ -93,25 +93,26 @@ def test_gpu_c5_view_full_size_parity(rend, c4):
 
 
 def test_gpu_c4_view_vs_compiled_reference(rend, c4):
-    """The C5 trajectory view of the 5M-surfel C4 scene against THE REFERENCE'S OWN render_into
-    (oracle/_ref, raster.cpp compiled unchanged; AABB binning, identical planes): blend counts,
-    ins_argmax and blended_total exact, fp32 planes within 1e-4 of the reference's fp64 planes."""
+    """The C4 frame (street camera) and a C5 trajectory view of the 5M-surfel scene against THE
+    REFERENCE'S OWN render_into (oracle/_ref, raster.cpp compiled unchanged; AABB binning, identical
+    planes): blend counts, ins_argmax and blended_total exact, fp32 planes within 1e-4 of the
+    reference's fp64 planes."""
     from oracle import pyref as R
     if not R.available():
         pytest.skip("oracle/_ref not built")
-    sc, _, _ = c4
-    cam = trajectory_cameras(256, 1920, 1080, first=160, count=1)[0]
-    g = rend.render(sc, None, cam, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=16))
+    sc, _, street_cam = c4
     rs = R.RefScene(sc.surfels, sc.f_sem, None)
     try:
-        r = rs.render(cam, RasterConfig(binning=Binning.Aabb, blending=Blending.TopK, top_k=16))
+        for cam in (street_cam, trajectory_cameras(256, 1920, 1080, first=160, count=1)[0]):
+            g = rend.render(sc, None, cam, RasterConfig(binning=Binning.Ellipse, blending=Blending.TopK, top_k=16))
+            r = rs.render(cam, RasterConfig(binning=Binning.Aabb, blending=Blending.TopK, top_k=16))
+            assert g.blended_total == r["blended_total"]
+            assert np.array_equal(g.blend_count, r["blend_count"]) and np.array_equal(g.ins_argmax, r["ins_argmax"])
+            for k in ("color", "depth", "normal", "alpha_acc", "sem_feat"):
+                err = np.max(np.abs(getattr(g, k).astype(np.float64) - r[k]))
+                assert err <= 1e-4, (k, err)
     finally:
         rs.close()
-    assert g.blended_total == r["blended_total"]
-    assert np.array_equal(g.blend_count, r["blend_count"]) and np.array_equal(g.ins_argmax, r["ins_argmax"])
-    for k in ("color", "depth", "normal", "alpha_acc", "sem_feat"):
-        err = np.max(np.abs(getattr(g, k).astype(np.float64) - r[k]))
-        assert err <= 1e-4, (k, err)
 
 
 @pytest.mark.parametrize("c_sem", [96, 128, 256, 100, 127, 129, 200])
