@@ -168,24 +168,29 @@ def repo_libs():
 
 class CpuReference:
     """The reference CPU renderer on the host cores. Preferred: oracle/_ref, the reference's own
-    raster.cpp / math_util.cpp / core_types.cpp compiled unchanged (kind "reference"): render_into
-    into persistent targets, serial project + bin, std::thread tile loop (raster.cpp:273-511), glibc exp.
-    For render_panoptic (c3p; panoptic.cpp / metrics.cpp are not compiled into _ref) and where _ref is
-    absent: the oracle restatement built with glibc exp (kind "port")."""
+    sources compiled unchanged (kind "reference"): render_into into persistent targets (raster.cpp /
+    math_util.cpp / core_types.cpp: serial project + bin, std::thread tile loop, raster.cpp:273-511,
+    glibc exp), or for c3p render_panoptic (metrics.cpp:339-369 with panoptic.cpp's assign_labels)
+    over a scene built once. Where _ref is absent: the oracle restatement built with glibc exp
+    (kind "port")."""
 
     def __init__(self, surfels, f_sem, f_ins=None, queries=None):
         from oracle import pyref as R
+        from paper_2604_10982_b200.raster import SceneMap
         self.queries = queries
-        self.kind = "reference" if (R.available() and not queries) else "port"
+        self.kind = "reference" if R.available() else "port"
         if self.kind == "reference":
-            self.rs = R.RefScene(surfels, f_sem, None)
+            self.rs = (R.RefPanopticScene(SceneMap(surfels, f_sem, f_ins, queries)) if queries
+                       else R.RefScene(surfels, f_sem, None))
         else:
-            from paper_2604_10982_b200.raster import SceneMap
             self.scene = SceneMap(surfels, f_sem, f_ins, queries)
 
     def frame(self, cam_c, cfg):
         if self.kind == "reference":
-            self.rs.render_into(cam_c, cfg.to_c())
+            if self.queries:
+                self.rs.render(cam_c, cfg.to_c())
+            else:
+                self.rs.render_into(cam_c, cfg.to_c())
             return
         from oracle import pyoracle as O
         from paper_2604_10982_b200.raster import Camera
@@ -204,9 +209,14 @@ class CpuReference:
         return times
 
     def describe(self, frames, w, h, n, threads):
-        what = ("the reference's raster.cpp/math_util.cpp/core_types.cpp compiled unchanged (oracle/_ref, "
-                "minimal Eigen stand-in), render_into into persistent targets" if self.kind == "reference" else
-                "reference algorithm restated in C++ (oracle), glibc exp")
+        if self.kind == "reference" and self.queries:
+            what = ("the reference's render_panoptic (metrics.cpp with panoptic.cpp's assign_labels and raster.cpp's "
+                    "render) compiled unchanged (oracle/_ref, minimal Eigen stand-in), scene built once")
+        elif self.kind == "reference":
+            what = ("the reference's raster.cpp/math_util.cpp/core_types.cpp compiled unchanged (oracle/_ref, "
+                    "minimal Eigen stand-in), render_into into persistent targets")
+        else:
+            what = "reference algorithm restated in C++ (oracle), glibc exp"
         return (f"{frames} full {w}x{h} frames of {n} surfels, best-of; {what}; serial project+bin, "
                 f"{threads} std::threads over tiles")
 

@@ -75,6 +75,10 @@ def load():
         "ref_assign_labels": (C.c_int, [vp, C.c_int64, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp]),
         "ref_render_panoptic": (C.c_int, [vp, C.c_int64, vp, C.c_int32, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp,
                                           P(A.psm_camera), P(A.psm_raster_config), vp, vp, vp]),
+        "ref_panoptic_scene_create": (vp, [vp, C.c_int64, vp, C.c_int32, vp, C.c_int32, C.c_int32, vp, vp, vp, vp,
+                                           vp]),
+        "ref_panoptic_scene_free": (None, [vp]),
+        "ref_render_panoptic_h": (C.c_int, [vp, P(A.psm_camera), P(A.psm_raster_config), vp, vp, vp]),
         "ref_project_surfel_backward": (C.c_int, [vp, P(A.psm_camera), P(A.psm_raster_config), vp, vp, vp, vp]),
         "ref_pipeline_backward": (C.c_int, [vp, P(A.psm_camera), P(A.psm_raster_config), C.c_int32, vp, vp,
                                             C.c_double, C.c_double, C.c_double, C.c_double, P(A.psm_scene_grads),
@@ -263,6 +267,38 @@ def assign_labels(surfels13, f_ins, queries):
                                 _p(arg)) != 0:
         raise ValueError("assign_labels failed")
     return dist, arg
+
+
+class RefPanopticScene:
+    """A panoptic psimap::SceneMap (f_sem, f_ins, instance queries) held by the reference library, so
+    that render_panoptic (metrics.cpp:339-369: assign_labels, render, epilogue) can be timed alone."""
+
+    def __init__(self, scene):
+        self.lib = load()
+        s = np.ascontiguousarray(scene.surfels)
+        f = np.ascontiguousarray(scene.f_sem)
+        fi = np.ascontiguousarray(scene.f_ins)
+        feat, mean, cov, alive, cls = _queries(scene.queries, fi.shape[1])
+        self._keep = (s, f, fi, feat, mean, cov, alive, cls)
+        self.h = self.lib.ref_panoptic_scene_create(_p(s), s.shape[0], _p(f), f.shape[1], _p(fi), fi.shape[1],
+                                                    len(scene.queries), _p(feat), _p(mean), _p(cov), _p(alive),
+                                                    _p(cls))
+
+    def render(self, cam_c, cfg_c, out=None) -> None:
+        ids, classes, sem = (None, None, None) if out is None else out
+        if self.lib.ref_render_panoptic_h(self.h, C.byref(cam_c), C.byref(cfg_c), _p(ids), _p(classes), _p(sem)) != 0:
+            raise ValueError("render_panoptic failed")
+
+    def close(self):
+        if self.h:
+            self.lib.ref_panoptic_scene_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def render_panoptic(scene, cam, cfg) -> dict:

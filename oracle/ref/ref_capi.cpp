@@ -368,6 +368,30 @@ int ref_render_panoptic(const double* surfels13, int64_t n, const double* f_sem,
   return PSM_OK;
 }
 
+// A panoptic SceneMap (f_sem, f_ins, queries) built once, for timing render_panoptic alone.
+void* ref_panoptic_scene_create(const double* surfels13, int64_t n, const double* f_sem, int32_t c_sem,
+                                const double* f_ins, int32_t c_ins, int32_t n_queries, const double* q_feat,
+                                const double* q_mean, const double* q_cov, const int32_t* q_alive,
+                                const int32_t* q_class) {
+  return new SceneMap(panoptic_scene(surfels13, n, f_sem, c_sem, f_ins, c_ins, n_queries, q_feat, q_mean, q_cov,
+                                     q_alive, q_class));
+}
+void ref_panoptic_scene_free(void* h) { delete static_cast<SceneMap*>(h); }
+
+// render_panoptic (metrics.cpp:339-369) over a scene built by ref_panoptic_scene_create.
+int ref_render_panoptic_h(void* h, const psm_camera* cam, const psm_raster_config* cfg, int32_t* ids,
+                          int32_t* classes, int32_t* sem_classes) {
+  try {
+    const PanopticRender pr = render_panoptic(*static_cast<SceneMap*>(h), to_cam(cam), to_cfg(cfg));
+    put(ids, pr.ids);
+    put(classes, pr.classes);
+    put(sem_classes, pr.sem_classes);
+  } catch (const std::invalid_argument&) {
+    return PSM_EINVAL;
+  }
+  return PSM_OK;
+}
+
 // ---- backward row (F4)
 
 // project_surfel_backward (raster.cpp:179-203) of one surfel under its own projection:
