@@ -734,7 +734,11 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     // iteration and halves the argmax reductions per pixel
     constexpr int kLP = PANO_T <= 3 ? 8 : (PANO_T <= 4 ? 16 : 32);
     constexpr int kPPI = 32 / kLP;
-    constexpr int kCPL = PANO_T * 32 / kLP;  // channels per lane: c = sub + kLP * t
+    constexpr int kCPL = PANO_T * 32 / kLP;  // channels per lane: c = chan(t), in pairs
+    static_assert(kCPL % 2 == 0, "channel pairs");
+    // lane sub holds the channel pairs 2 (sub + kLP j) + {0, 1}, j < kCPL / 2 (monotone in t)
+#define PSM_PANO_CHAN(t) (2 * (sub + kLP * ((t) >> 1)) + ((t) & 1))
+    const bool vec2 = (D & 1) == 0;  // even rows: 16-byte aligned pairs, one load each
     const int grp = lane / kLP, sub = lane % kLP;
     for (int q0 = 0; q0 < 32; q0 += kPPI) {
       const int q = q0 + grp;
@@ -770,12 +774,25 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
             const double w = __shfl_sync(0xffffffffu, sw, grp * kLP + i);
             if (qgate && i0 + i < nq && D > 0) {
               const double* row = p.feat64 + static_cast<int64_t>(s_i) * D;
+              const bool first = i0 + i == 0;
+              if (vec2) {
 #pragma unroll
-              for (int t = 0; t < kCPL; ++t) {
-                const int c = sub + kLP * t;
-                if (c < D) {
-                  const double v = __ldg(row + c);
-                  acc[t] = i0 + i == 0 ? w * v : acc[t] + w * v;
+                for (int j = 0; j < kCPL / 2; ++j) {
+                  const int c = PSM_PANO_CHAN(2 * j);
+                  if (c < D) {
+                    const double2 v = __ldg(reinterpret_cast<const double2*>(row + c));
+                    acc[2 * j] = first ? w * v.x : acc[2 * j] + w * v.x;
+                    acc[2 * j + 1] = first ? w * v.y : acc[2 * j + 1] + w * v.y;
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int t = 0; t < kCPL; ++t) {
+                  const int c = PSM_PANO_CHAN(t);
+                  if (c < D) {
+                    const double v = __ldg(row + c);
+                    acc[t] = first ? w * v : acc[t] + w * v;
+                  }
                 }
               }
             }
@@ -790,7 +807,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
             const double* row = p.feat64 + static_cast<int64_t>(__ldg(p.vals + pos)) * D;
 #pragma unroll
             for (int t = 0; t < kCPL; ++t) {
-              const int c = sub + kLP * t;
+              const int c = PSM_PANO_CHAN(t);
               if (c < D) {
                 const double v = __ldg(row + c);
                 acc[t] = i == 0 ? w * v : acc[t] + w * v;
@@ -805,7 +822,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       bool hs = false, hi = false;
 #pragma unroll
       for (int t = 0; t < kCPL; ++t) {
-        const int c = sub + kLP * t;
+        const int c = PSM_PANO_CHAN(t);
         if (c < cs) {
           if (!hs || acc[t] > bs) bs = acc[t];
           hs = true;
@@ -826,7 +843,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       unsigned fs = 0xffffffffu, fi = 0xffffffffu;  // this lane's lowest channel holding the maximum
 #pragma unroll
       for (int t = kCPL - 1; t >= 0; --t) {
-        const int c = sub + kLP * t;
+        const int c = PSM_PANO_CHAN(t);
         if (c < cs && acc[t] == bs) fs = static_cast<unsigned>(c);
         else if (c >= cs && c < D && acc[t] == bi) fi = static_cast<unsigned>(c - cs);
       }
@@ -847,7 +864,7 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
       if (planes) {  // raster.cpp:486-498: zeros (and -1) where nothing blended
 #pragma unroll
         for (int t = 0; t < kCPL; ++t) {
-          const int c = sub + kLP * t;
+          const int c = PSM_PANO_CHAN(t);
           const float v = nq > 0 ? static_cast<float>(acc[t]) : 0.f;
           if (c < cs) {
             if (p.sem_feat) p.sem_feat[qpix * cs + c] = v;
@@ -869,6 +886,8 @@ __device__ __forceinline__ void blend_block(const BlendParams& p, const int tile
     }
   }
 }
+
+#undef PSM_PANO_CHAN
 
 // Persistent CTAs (resident count per SM x SMs): each warp pulls (tile, 8x4 block) items
 // from the launch's work counter until the tiles run out, so an SM's slots are never held
