@@ -122,7 +122,7 @@ def test_gpu_render_panoptic_c3p_full_size(rend):
             assert np.array_equal(getattr(g, k), r[k]), k
 
 
-@pytest.mark.parametrize("c_sem,n_q", [(8, 16), (64, 40), (128, 64), (256, 100), (3, 5)])
+@pytest.mark.parametrize("c_sem,n_q", [(8, 16), (64, 40), (128, 64), (256, 100), (3, 5), (7, 4), (33, 30), (61, 40)])
 @pytest.mark.parametrize("blending,k", [(Blending.TopK, 8), (Blending.TopK, 32), (Blending.Full, 16)])
 def test_gpu_render_panoptic_feature_widths(rend, c_sem, n_q, blending, k):
     """The fp64 panoptic phase at every lane shape (8 lanes per pixel up to 96 channels, 16 up to 128,
